@@ -1,0 +1,248 @@
+// Shared device/host definitions for libflowreg_b200 (sm_100a).
+//
+// Layout (fields.py:162,190,237): every field is C-order over
+// (n0, n1, n2), last axis fastest.  2D grids are stored as (1, n0, n1): the
+// size-1 leading axis is exact under every operator (interp weights (0,1,0,0),
+// FD8 differences vanish, DFT frequency 0).  A vector field has d components
+// (d = 2 or 3); component c differentiates / displaces along grid axis
+// (3 - d) + c.  Time series are (n_t + 1, n0, n1, n2).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace frg {
+
+struct Dims {
+    int n0, n1, n2;  // n0 == 1 for 2D grids
+    long long N;     // n0 * n1 * n2
+    int d;           // vector components (2 or 3)
+    __host__ __device__ int axis_len(int a) const { return a == 0 ? n0 : (a == 1 ? n1 : n2); }
+    __host__ __device__ int comp_axis(int c) const { return (3 - d) + c; }
+};
+
+inline Dims make_dims(const int32_t n[3], int d) {
+    Dims g;
+    g.n0 = n[0];
+    g.n1 = n[1];
+    g.n2 = n[2];
+    g.N = (long long)g.n0 * g.n1 * g.n2;
+    g.d = d;
+    return g;
+}
+
+enum Method { NEAREST = 0, LINEAR = 1, CUBIC = 2 };
+enum DType { F32 = 0, F64 = 1, I32 = 2 };
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// status codes of the C-ABI (include/flowreg_b200.h)
+constexpr int OK = 0;
+constexpr int E_ARG = -1;
+constexpr int E_NONFINITE = -2;
+constexpr int E_CUDA = -3;
+constexpr int E_CUFFT = -4;
+constexpr int E_STATE = -5;
+
+#define FRG_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            throw ::frg::Error(::frg::E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define FRG_CHECK_LAUNCH() FRG_CUDA(cudaGetLastError())
+
+#define FRG_REQUIRE(cond, msg)                                \
+    do {                                                      \
+        if (!(cond)) throw ::frg::Error(::frg::E_ARG, (msg)); \
+    } while (0)
+
+constexpr double TWO_PI = 6.283185307179586476925286766559;
+
+// number of SMs on B200; grids for grid-stride kernels are multiples of it
+constexpr int NUM_SMS = 148;
+
+inline int blocks_for(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return (int)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------------------
+// periodic index helpers
+// ---------------------------------------------------------------------------
+
+// floor-mod of an integer (Python semantics, _kernels.py:107-118)
+__host__ __device__ __forceinline__ int pmod(long long i, int n) {
+    long long r = i % n;
+    return (int)(r < 0 ? r + n : r);
+}
+
+template <typename T>
+struct Real;
+template <>
+struct Real<float> {
+    __device__ __forceinline__ static float floor_(float x) { return floorf(x); }
+};
+template <>
+struct Real<double> {
+    __device__ __forceinline__ static double floor_(double x) { return floor(x); }
+};
+
+// Lagrange cubic weights for nodes at offsets -1, 0, 1, 2 (_kernels.py:162-167)
+template <typename T>
+__device__ __forceinline__ void lagrange4(T t, T w[4]) {
+    const T one = T(1), two = T(2);
+    w[0] = -t * (t - one) * (t - two) / T(6);
+    w[1] = (t + one) * (t - one) * (t - two) / two;
+    w[2] = -(t + one) * t * (t - two) / two;
+    w[3] = (t + one) * t * (t - one) / T(6);
+}
+
+// Per-axis stencil: wrapped node indices (already multiplied by the axis
+// stride) and weights.  NT = taps per axis (1 nearest, 2 linear, 4 cubic).
+template <typename T, int NT>
+struct Axis {
+    int off[NT];
+    T w[NT];
+};
+
+// Build the axis stencil for fractional position base + frac where `base` is
+// an integer node index (may be outside [0, n)) and frac in [0, 1).
+template <typename T, int M>
+__device__ __forceinline__ void axis_stencil(long long fl, T t, int n, int stride,
+                                             Axis<T, (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1))>& ax) {
+    if (M == NEAREST) {
+        // caller passes fl = floor(q + 0.5), t unused
+        ax.off[0] = pmod(fl, n) * stride;
+        ax.w[0] = T(1);
+    } else if (M == LINEAR) {
+        int i0 = pmod(fl, n);
+        int i1 = i0 + 1;
+        if (i1 >= n) i1 -= n;
+        ax.off[0] = i0 * stride;
+        ax.off[1] = i1 * stride;
+        ax.w[0] = T(1) - t;
+        ax.w[1] = t;
+    } else {
+        T w[4];
+        lagrange4(t, w);
+        if (n == 1) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                ax.off[a] = 0;
+                ax.w[a] = w[a];
+            }
+        } else {
+            int b = pmod(fl - 1, n);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                int x = b + a;
+                if (x >= n) x -= n;
+                if (x >= n) x -= n;  // n >= 2 covers every n the grids allow
+                ax.off[a] = x * stride;
+                ax.w[a] = w[a];
+            }
+        }
+    }
+}
+
+template <int M>
+struct Taps {
+    static constexpr int value = (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1));
+};
+
+// Full tensor-product stencil for one query point.
+template <typename T, int M>
+struct Stencil {
+    Axis<T, Taps<M>::value> a0, a1, a2;
+};
+
+// Query point given as fractional indices (q0, q1, q2) in the storage type
+// accuracy of `T` (double for the generic sample_nd boundary).
+template <typename T, int M>
+__device__ __forceinline__ void make_stencil_q(const Dims& g, T q0, T q1, T q2, Stencil<T, M>& s) {
+    if (M == NEAREST) {
+        axis_stencil<T, M>((long long)Real<T>::floor_(q0 + T(0.5)), T(0), g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>((long long)Real<T>::floor_(q1 + T(0.5)), T(0), g.n1, g.n2, s.a1);
+        axis_stencil<T, M>((long long)Real<T>::floor_(q2 + T(0.5)), T(0), g.n2, 1, s.a2);
+    } else {
+        T f0 = Real<T>::floor_(q0), f1 = Real<T>::floor_(q1), f2 = Real<T>::floor_(q2);
+        axis_stencil<T, M>((long long)f0, q0 - f0, g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>((long long)f1, q1 - f1, g.n1, g.n2, s.a1);
+        axis_stencil<T, M>((long long)f2, q2 - f2, g.n2, 1, s.a2);
+    }
+}
+
+// Query point = grid node (i, j, k) + displacement (in index units).  The
+// integer part is split off exactly, so precision does not degrade with n.
+template <typename T, int M>
+__device__ __forceinline__ void make_stencil_disp(const Dims& g, int i, int j, int k, T d0, T d1, T d2,
+                                                  Stencil<T, M>& s) {
+    if (M == NEAREST) {
+        axis_stencil<T, M>(i + (long long)Real<T>::floor_(d0 + T(0.5)), T(0), g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>(j + (long long)Real<T>::floor_(d1 + T(0.5)), T(0), g.n1, g.n2, s.a1);
+        axis_stencil<T, M>(k + (long long)Real<T>::floor_(d2 + T(0.5)), T(0), g.n2, 1, s.a2);
+    } else {
+        T f0 = Real<T>::floor_(d0), f1 = Real<T>::floor_(d1), f2 = Real<T>::floor_(d2);
+        axis_stencil<T, M>(i + (long long)f0, d0 - f0, g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>(j + (long long)f1, d1 - f1, g.n1, g.n2, s.a1);
+        axis_stencil<T, M>(k + (long long)f2, d2 - f2, g.n2, 1, s.a2);
+    }
+}
+
+// Apply a stencil to one field.  Accumulation order mirrors the reference:
+// innermost over the last axis, then axis 1, then axis 0 (_kernels.py:207-219).
+template <typename A, typename T, int M, typename V>
+__device__ __forceinline__ A apply_stencil(const V* __restrict__ f, const Stencil<T, M>& s) {
+    constexpr int NT = Taps<M>::value;
+    if (M == NEAREST) {
+        return (A)__ldg(f + (long long)s.a0.off[0] + s.a1.off[0] + s.a2.off[0]);
+    } else if (M == LINEAR) {
+        A c[2][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const V* row = f + (long long)s.a0.off[a] + s.a1.off[b];
+                c[a][b] = (A(1) - (A)s.a2.w[1]) * (A)__ldg(row + s.a2.off[0]) +
+                          (A)s.a2.w[1] * (A)__ldg(row + s.a2.off[1]);
+            }
+        A t1 = (A)s.a1.w[1], t0 = (A)s.a0.w[1];
+        return (A(1) - t0) * ((A(1) - t1) * c[0][0] + t1 * c[0][1]) +
+               t0 * ((A(1) - t1) * c[1][0] + t1 * c[1][1]);
+    } else {
+        A acc = A(0);
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+            A plane = A(0);
+#pragma unroll
+            for (int b = 0; b < NT; ++b) {
+                const V* row = f + (long long)s.a0.off[a] + s.a1.off[b];
+                A r = A(0);
+#pragma unroll
+                for (int c = 0; c < NT; ++c) r += (A)s.a2.w[c] * (A)__ldg(row + s.a2.off[c]);
+                plane += (A)s.a1.w[b] * r;
+            }
+            acc += (A)s.a0.w[a] * plane;
+        }
+        return acc;
+    }
+}
+
+// flat index -> (i, j, k)
+__device__ __forceinline__ void unflatten(const Dims& g, long long p, int& i, int& j, int& k) {
+    k = (int)(p % g.n2);
+    long long r = p / g.n2;
+    j = (int)(r % g.n1);
+    i = (int)(r / g.n1);
+}
+
+}  // namespace frg

@@ -1,0 +1,577 @@
+// Reduced-space KKT context: the B200-native KktState (kkt.py:136-341).
+//
+// The context owns every per-velocity byproduct in HBM: departure maps
+// (stored as index-unit displacements), state / adjoint series, state
+// gradients on the mesh AND gathered at the forward feet (grad m_j(y), reused
+// by every Hessian matvec), the adjoint multiplier, plus cuFFT plans and
+// spectral workspaces.  Transport fields use transport_dtype; velocity-space
+// vectors (v, gradient, PCG vectors, spectral regularisation) use
+// control_dtype, so H2/H3 keeps fp64 control vectors (SURVEY.md §7 hard part 1)
+// while the transport runs in fp32.
+#include <cmath>
+#include <vector>
+
+#include "kkt.h"
+
+namespace frg {
+
+static size_t es(int dt) { return dt == F64 ? 8 : 4; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b) {
+        if (b > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            FRG_CUDA(cudaMalloc(&p, b));
+            bytes = b;
+        }
+    }
+    void free_() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T = char>
+    T* at(size_t byte_off = 0) const {
+        return (T*)((char*)p + byte_off);
+    }
+};
+
+struct KktCtx {
+    Dims g;
+    int n_t, method, scheme, distance, tdt, cdt;
+    RegSpec reg;
+    cudaStream_t st;
+    PlanCache plans;
+    Workspace ws_a, ws_b, ws_c;
+    DevBuf m0, m1, v, vT, negv, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
+    DevBuf vtT, vty, mt, lt, bf, disp_trial, mtrial, gmC, tmp1, tmp2, tmp3;
+    // two-level coarse pieces
+    DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
+    bool coarse_ready = false, h0_ready = false;
+    bool have_images = false, have_state = false;
+    double initial_mismatch = 0.0, dist_cur = 0.0;
+    bool dist_valid = false;
+    long long matvecs = 0, pde_solves = 0, precond_fallbacks = 0;
+
+    size_t T() const { return es(tdt); }
+    size_t C() const { return es(cdt); }
+    long long N() const { return g.N; }
+    double cell_volume() const {
+        double v = 1.0;
+        for (int c = 0; c < g.d; ++c) v *= TWO_PI / g.axis_len(g.comp_axis(c));
+        return v;
+    }
+};
+
+KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance, int tdt, int cdt, const RegSpec& reg,
+                   cudaStream_t st) {
+    FRG_REQUIRE(g.d == 2 || g.d == 3, "d must be 2 or 3");
+    FRG_REQUIRE((g.d == 2) == (g.n0 == 1), "2D grids are passed as n = {1, n0, n1}");
+    FRG_REQUIRE(n_t >= 1, "n_t must be >= 1");
+    FRG_REQUIRE(method >= 0 && method <= 2, "unknown interpolation method");
+    FRG_REQUIRE(scheme == 0 || scheme == 1, "unknown derivative scheme");
+    FRG_REQUIRE(distance == 0 || distance == 1, "unknown distance measure");
+    FRG_REQUIRE(tdt == F32 || tdt == F64, "transport dtype must be f32 or f64");
+    FRG_REQUIRE(cdt == F32 || cdt == F64, "control dtype must be f32 or f64");
+    FRG_REQUIRE(!(tdt == F64 && cdt == F32), "transport precision may not exceed control precision");
+    FRG_REQUIRE(reg.alpha > 0, "alpha must be positive");
+    auto* k = new KktCtx();
+    k->g = g;
+    k->n_t = n_t;
+    k->method = method;
+    k->scheme = scheme;
+    k->distance = distance;
+    k->tdt = tdt;
+    k->cdt = cdt;
+    k->reg = reg;
+    k->st = st;
+    const long long N = g.N, d = g.d;
+    const size_t T = k->T(), C = k->C();
+    k->m0.alloc(N * T);
+    k->m1.alloc(N * T);
+    k->v.alloc(d * N * C);
+    k->vT.alloc(d * N * T);
+    k->negv.alloc(d * N * T);
+    k->disp_f.alloc(d * N * T);
+    k->disp_b.alloc(d * N * T);
+    k->divv.alloc(N * T);
+    k->cmul.alloc(N * T);
+    k->mseries.alloc((n_t + 1) * N * T);
+    k->grads.alloc((n_t + 1) * d * N * T);
+    k->grads_y.alloc(n_t * d * N * T);
+    k->lam.alloc((n_t + 1) * N * T);
+    k->vtT.alloc(d * N * T);
+    k->vty.alloc(d * N * T);
+    k->mt.alloc(2 * N * T);
+    k->lt.alloc((n_t + 1) * N * T);
+    k->bf.alloc(d * N * T);
+    k->disp_trial.alloc(d * N * T);
+    k->mtrial.alloc(2 * N * T);
+    size_t sa = (size_t)half_len(g) * (C == 8 ? 16 : 8) * d + (size_t)half_len(g) * 8;
+    size_t sb = (size_t)half_len(g) * (T == 8 ? 16 : 8) * d;
+    k->ws_a.get(sa);
+    k->ws_b.get(sb);
+    return k;
+}
+
+void kkt_destroy(KktCtx* k) {
+    if (!k) return;
+    DevBuf* bufs[] = {&k->m0, &k->m1, &k->v, &k->vT, &k->negv, &k->disp_f, &k->disp_b, &k->divv, &k->cmul,
+                      &k->mseries, &k->grads, &k->grads_y, &k->lam, &k->vtT, &k->vty, &k->mt, &k->lt, &k->bf,
+                      &k->disp_trial, &k->mtrial, &k->gmC, &k->tmp1, &k->tmp2, &k->tmp3, &k->c_gm, &k->c_w,
+                      &k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q, &k->c_u};
+    for (DevBuf* b : bufs) b->free_();
+    k->ws_a.release();
+    k->ws_b.release();
+    k->ws_c.release();
+    k->plans.clear();
+    delete k;
+}
+
+void kkt_set_stream(KktCtx* k, cudaStream_t st) { k->st = st; }
+
+// ---------------------------------------------------------------------------
+// distance measures (distance.py:43-91) on transport-dtype fields
+// ---------------------------------------------------------------------------
+struct NccMoments {
+    double a, b, c;
+};
+
+static NccMoments ncc_moments(KktCtx* k, const void* md) {
+    double cv = k->cell_volume();
+    NccMoments m;
+    m.a = dot(k->tdt, k->m1.p, md, k->N(), k->st) * cv;
+    m.b = dot(k->tdt, md, md, k->N(), k->st) * cv;
+    m.c = dot(k->tdt, k->m1.p, k->m1.p, k->N(), k->st) * cv;
+    if (m.b <= 0.0 || m.c <= 0.0) throw Error(E_ARG, "ZeroNormError: normalized cross correlation needs nonzero images");
+    return m;
+}
+
+static double dist_value(KktCtx* k, const void* md) {
+    if (k->distance == 0) {
+        // 0.5 * |md - m1|^2 (quadrature weighted)
+        scale_diff(k->tdt, md, k->m1.p, 1.0, k->tmp1.p, k->N(), k->st);
+        return 0.5 * dot(k->tdt, k->tmp1.p, k->tmp1.p, k->N(), k->st) * k->cell_volume();
+    }
+    NccMoments m = ncc_moments(k, md);
+    return 1.0 - (m.a * m.a) / (m.b * m.c);
+}
+
+// lam_final = -(md - m1) or the NCC final condition (distance.py:57-65)
+static void adjoint_final(KktCtx* k, const void* md, void* out) {
+    if (k->distance == 0) {
+        scale_diff(k->tdt, md, k->m1.p, -1.0, out, k->N(), k->st);
+        return;
+    }
+    NccMoments m = ncc_moments(k, md);
+    double s = -2.0 * (m.a / (m.b * m.c));
+    // out = s * ((a/b) md - m1)
+    lincomb3(k->tdt, s * (m.a / m.b), md, -s, k->m1.p, 0.0, nullptr, out, k->N(), k->st);
+}
+
+// GN final condition (distance.py:68-91); SSD handled by the fused sign in inc_state
+static void incremental_final_ncc(KktCtx* k, const void* mt, const void* md, void* out) {
+    NccMoments m = ncc_moments(k, md);
+    double cv = k->cell_volume();
+    double mm = dot(k->tdt, md, mt, k->N(), k->st) * cv;
+    double rm = dot(k->tdt, k->m1.p, mt, k->N(), k->st) * cv;
+    double a = m.a, b = m.b, c = m.c;
+    double q1 = 2.0 * a * mm / (b * b) - rm / b;
+    double q2 = 4.0 * a * a * mm / (b * b * b) - 2.0 * a * rm / (b * b);
+    double q3 = a * a / (b * b);
+    lincomb3(k->tdt, (2.0 / c) * (-q1), k->m1.p, (2.0 / c) * q2, md, (2.0 / c) * (-q3), mt, out, k->N(), k->st);
+}
+
+void kkt_set_images(KktCtx* k, const void* m0, const void* m1, int dtype) {
+    convert(dtype, m0, k->tdt, k->m0.p, k->N(), k->st);
+    convert(dtype, m1, k->tdt, k->m1.p, k->N(), k->st);
+    k->tmp1.alloc(k->N() * k->T());
+    k->have_images = true;
+    k->initial_mismatch = dist_value(k, k->m0.p);
+}
+
+// velocity (control dtype, d x N) -> transport-dtype departure displacements
+static void departure_of(KktCtx* k, const void* vC, void* disp, void* scratchT, bool negate) {
+    const long long dN = (long long)k->g.d * k->N();
+    const void* src = vC;
+    int sdt = k->cdt;
+    if (negate || k->cdt != k->tdt) {
+        convert(k->cdt, vC, k->tdt, scratchT, dN, k->st);
+        if (negate) axpby(k->tdt, 0.0, scratchT, -1.0, scratchT, dN, k->st);
+        src = scratchT;
+        sdt = k->tdt;
+    }
+    departure(k->g, k->tdt, sdt, k->method, 1.0 / k->n_t, src, disp, k->st);
+}
+
+static void gradient_slices(KktCtx* k, int nslices, const void* u, void* out) {
+    if (k->scheme == 0) {
+        fd8_gradient(k->g, k->tdt, nslices, u, out, k->st);
+    } else {
+        const size_t T = k->T();
+        for (int s = 0; s < nslices; ++s)
+            spectral_gradient(k->g, k->tdt, (const char*)u + (size_t)s * k->N() * T,
+                              (char*)out + (size_t)s * k->g.d * k->N() * T, k->st);
+    }
+}
+
+void kkt_refresh(KktCtx* k, const void* v) {
+    FRG_REQUIRE(k->have_images, "set_images must precede refresh");
+    const long long N = k->N(), d = k->g.d;
+    const size_t T = k->T(), C = k->C();
+    cudaStream_t st = k->st;
+    FRG_CUDA(cudaMemcpyAsync(k->v.p, v, d * N * C, cudaMemcpyDeviceToDevice, st));
+    // vT = v in transport precision (departure + divergence)
+    convert(k->cdt, k->v.p, k->tdt, k->vT.p, d * N, st);
+    departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->vT.p, k->disp_f.p, st);   // kkt.py:171
+    axpby(k->tdt, -1.0, k->vT.p, 0.0, k->negv.p, d * N, st);
+    departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->negv.p, k->disp_b.p, st); // kkt.py:172
+    if (k->scheme == 0)                                                                     // kkt.py:173
+        fd8_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
+    else
+        spectral_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
+    FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
+    solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);         // kkt.py:174
+    gradient_slices(k, k->n_t + 1, k->mseries.p, k->grads.p);                              // kkt.py:175
+    {
+        // grad m_j at the forward feet, reused by every matvec (transport.py:172)
+        std::vector<const void*> in(d * k->n_t);
+        std::vector<void*> out(d * k->n_t);
+        for (long long e = 0; e < d * k->n_t; ++e) {
+            in[e] = k->grads.at<char>(e * N * T);
+            out[e] = k->grads_y.at<char>(e * N * T);
+        }
+        gather_fields(k->g, k->tdt, k->method, k->disp_f.p, (int)(d * k->n_t), in.data(), out.data(), st);
+    }
+    adjoint_multiplier(k->g, k->tdt, k->method, 1.0 / k->n_t, k->disp_b.p, k->divv.p, k->cmul.p, st);
+    void* m_final = k->mseries.at<char>((size_t)k->n_t * N * T);
+    void* lam_final = k->lam.at<char>((size_t)k->n_t * N * T);
+    adjoint_final(k, m_final, lam_final);                                                  // kkt.py:176
+    solve_adjoint(k->g, k->tdt, k->method, k->n_t, k->disp_b.p, k->cmul.p, k->lam.p, st);  // kkt.py:177-184
+    k->pde_solves += 2;
+    k->have_state = true;
+    k->dist_valid = false;
+    k->coarse_ready = false;
+    k->h0_ready = false;
+}
+
+static const void* m_final(KktCtx* k) { return k->mseries.at<char>((size_t)k->n_t * k->N() * k->T()); }
+
+static double current_dist(KktCtx* k) {
+    if (!k->dist_valid) {
+        k->dist_cur = dist_value(k, m_final(k));
+        k->dist_valid = true;
+    }
+    return k->dist_cur;
+}
+
+static double reg_energy_c(KktCtx* k, const void* vC) {
+    size_t need = spectral_ws_bytes(k->g, k->cdt, k->g.d);
+    return reg_energy_ex(k->plans, k->ws_a.get(need), k->g, k->cdt, vC, k->reg, k->st);
+}
+
+double kkt_objective(KktCtx* k) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    return current_dist(k) + reg_energy_c(k, k->v.p);
+}
+
+double kkt_objective_at(KktCtx* k, const void* v_trial) {
+    FRG_REQUIRE(k->have_images, "set_images first");
+    const long long N = k->N();
+    const size_t T = k->T();
+    // fresh trajectory + state solve keeping only two slices (kkt.py:201-205)
+    departure_of(k, v_trial, k->disp_trial.p, k->vtT.p, false);
+    FRG_CUDA(cudaMemcpyAsync(k->mtrial.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, k->st));
+    for (int j = 0; j < k->n_t; ++j) {
+        const void* in = k->mtrial.at<char>((size_t)(j & 1) * N * T);
+        void* out = k->mtrial.at<char>((size_t)((j + 1) & 1) * N * T);
+        gather_fields(k->g, k->tdt, k->method, k->disp_trial.p, 1, &in, &out, k->st);
+    }
+    k->pde_solves += 1;
+    const void* mfin = k->mtrial.at<char>((size_t)(k->n_t & 1) * N * T);
+    return dist_value(k, mfin) + reg_energy_c(k, v_trial);
+}
+
+// out = alpha L a + P[b_T]  (kkt.py:233-235, 259-260)
+static void reg_plus_body(KktCtx* k, const void* a, const void* bT, void* out) {
+    size_t sa = (size_t)half_len(k->g) * (k->C() == 8 ? 16 : 8) * k->g.d + (size_t)half_len(k->g) * 8;
+    size_t sb = (size_t)half_len(k->g) * (k->T() == 8 ? 16 : 8) * k->g.d;
+    reg_plus_project_ex(k->plans, k->ws_a.get(sa), k->ws_b.get(sb), k->g, k->cdt, a, k->tdt, bT, out, k->reg,
+                        k->reg.incomp != 0, k->st);
+}
+
+void kkt_gradient(KktCtx* k, void* g_out) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    body_force(k->g, k->tdt, k->tdt, k->n_t, k->lam.p, k->grads.p, k->bf.p, false, k->st);
+    reg_plus_body(k, k->v.p, k->bf.p, g_out);
+}
+
+void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    const long long N = k->N();
+    const size_t T = k->T();
+    void* lt_final = k->lt.at<char>((size_t)k->n_t * N * T);
+    if (k->distance == 0) {
+        // SSD: lam~(1) = -m~(1), fused into the last incremental step (distance.py:80-81)
+        inc_state(k->g, k->tdt, k->cdt, k->method, k->n_t, k->disp_f.p, k->grads.p, k->grads_y.p, vt, k->vtT.p,
+                  k->vty.p, k->mt.p, lt_final, -1.0, false, k->st);
+    } else {
+        inc_state(k->g, k->tdt, k->cdt, k->method, k->n_t, k->disp_f.p, k->grads.p, k->grads_y.p, vt, k->vtT.p,
+                  k->vty.p, k->mt.p, k->tmp1.p, 1.0, false, k->st);
+        incremental_final_ncc(k, k->tmp1.p, m_final(k), lt_final);
+    }
+    solve_adjoint(k->g, k->tdt, k->method, k->n_t, k->disp_b.p, k->cmul.p, k->lt.p, k->st);
+    k->matvecs += 1;
+    k->pde_solves += 2;
+    body_force(k->g, k->tdt, k->tdt, k->n_t, k->lt.p, k->grads.p, k->bf.p, false, k->st);
+    reg_plus_body(k, vt, k->bf.p, out);
+}
+
+double kkt_mismatch(KktCtx* k) {
+    if (k->initial_mismatch == 0.0) return 0.0;
+    return current_dist(k) / k->initial_mismatch;
+}
+
+double kkt_initial_mismatch(KktCtx* k) { return k->initial_mismatch; }
+
+// kkt.py:207-218 — 0.5 beta (<w, w> + <grad w, grad w>), spectral gradient
+double kkt_divergence_energy(KktCtx* k) {
+    if (k->reg.incomp != 2) return 0.0;
+    const long long N = k->N();
+    k->tmp2.alloc((size_t)k->g.d * N * k->T());
+    spectral_gradient(k->g, k->tdt, k->divv.p, k->tmp2.p, k->st);
+    double cv = k->cell_volume();
+    double ww = dot(k->tdt, k->divv.p, k->divv.p, N, k->st) * cv;
+    double gg = dot(k->tdt, k->tmp2.p, k->tmp2.p, (long long)k->g.d * N, k->st) * cv;
+    return 0.5 * k->reg.beta * (ww + gg);
+}
+
+// ---------------------------------------------------------------------------
+// preconditioners (kkt.py:269-341)
+// ---------------------------------------------------------------------------
+static void apply_sym_c(KktCtx* k, const Dims& g, const void* in, void* out, int kind) {
+    size_t need = spectral_ws_bytes(g, k->cdt, g.d);
+    spectral_apply_ex(k->plans, k->ws_c.get(need), g, k->cdt, g.d, in, out, kind, k->reg, k->st);
+}
+
+static double l2(KktCtx* k, const Dims& g, const void* a, const void* b) {
+    double cv = 1.0;
+    for (int c = 0; c < g.d; ++c) cv *= TWO_PI / g.axis_len(g.comp_axis(c));
+    return dot(k->cdt, a, b, (long long)g.d * g.N, k->st) * cv;
+}
+
+// plain PCG for the nested solves (kkt.py:99-133); returns breakdown flag
+template <typename Op, typename Pre>
+static bool inner_pcg(KktCtx* k, const Dims& g, Op op, Pre pre, const void* rhs, void* x, void* r, void* z, void* s,
+                      void* q, double tol_rel, int max_it, int* iters) {
+    const long long n = (long long)g.d * g.N;
+    const int cdt = k->cdt;
+    fill(cdt, x, 0.0, n, k->st);
+    FRG_CUDA(cudaMemcpyAsync(r, rhs, n * k->C(), cudaMemcpyDeviceToDevice, k->st));
+    double rhs_norm = std::sqrt(std::max(l2(k, g, rhs, rhs), 0.0));
+    *iters = 0;
+    if (rhs_norm == 0.0) return false;
+    pre(r, z);
+    FRG_CUDA(cudaMemcpyAsync(s, z, n * k->C(), cudaMemcpyDeviceToDevice, k->st));
+    double rz = l2(k, g, r, z);
+    int it = 0;
+    double cv = 1.0;
+    for (int c = 0; c < g.d; ++c) cv *= TWO_PI / g.axis_len(g.comp_axis(c));
+    while (it < max_it) {
+        op(s, q);
+        double sq = l2(k, g, s, q);
+        if (!std::isfinite(sq) || sq <= 0.0) {
+            *iters = it;
+            return true;
+        }
+        double kap = rz / sq;
+        double rr = pcg_update(cdt, kap, s, q, x, r, n, k->st) * cv;
+        it += 1;
+        if (std::sqrt(std::max(rr, 0.0)) <= tol_rel * rhs_norm) break;
+        pre(r, z);
+        double rz_new = l2(k, g, r, z);
+        if (!std::isfinite(rz_new) || rz_new <= 0.0) {
+            *iters = it;
+            return true;
+        }
+        double mu = rz_new / rz;
+        rz = rz_new;
+        axpby(cdt, 1.0, z, mu, s, n, k->st);  // s = z + mu s
+    }
+    *iters = it;
+    return false;
+}
+
+static void ensure_h0(KktCtx* k) {
+    if (k->h0_ready) return;
+    const long long dN = (long long)k->g.d * k->N();
+    k->gmC.alloc(dN * k->C());
+    // grad m(1) with the state scheme == the last stored state gradient (kkt.py:269-272)
+    convert(k->tdt, k->grads.at<char>((size_t)k->n_t * dN * k->T()), k->cdt, k->gmC.p, dN, k->st);
+    k->h0_ready = true;
+}
+
+static void ensure_coarse(KktCtx* k) {
+    if (k->coarse_ready) return;
+    Dims gc = coarse_dims(k->g);
+    const long long Nc = gc.N, dNc = (long long)gc.d * Nc;
+    size_t C = k->C();
+    k->c_gm.alloc(dNc * C);
+    k->tmp3.alloc(k->N() * C);
+    k->c_u.alloc(Nc * C);
+    // coarse image: restrict(m(1)) in control precision, then its gradient (kkt.py:291-296)
+    convert(k->tdt, m_final(k), k->cdt, k->tmp3.p, k->N(), k->st);
+    restrict_field_ex(k->plans, k->ws_c.get(restrict_ws_bytes(k->g, k->cdt)), k->g, k->cdt, k->tmp3.p, k->c_u.p, k->st);
+    if (k->scheme == 0)
+        fd8_gradient(gc, k->cdt, 1, k->c_u.p, k->c_gm.p, k->st);
+    else
+        spectral_gradient(gc, k->cdt, k->c_u.p, k->c_gm.p, k->st);
+    k->coarse_ready = true;
+}
+
+void kkt_apply_precond(KktCtx* k, int kind, double outer_tol, double inner_tol_factor, int inner_max, const void* r,
+                       void* z, int* fell_back) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    *fell_back = 0;
+    const Dims& g = k->g;
+    const long long dN = (long long)g.d * g.N;
+    const size_t C = k->C();
+    if (kind == 0) {
+        apply_sym_c(k, g, r, z, SK_REG_INV);  // kkt.py:310-311
+        return;
+    }
+    double tol = inner_tol_factor * outer_tol;
+    int iters = 0;
+    if (kind == 1) {
+        ensure_h0(k);
+        DevBuf* bufs[] = {&k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q};
+        for (DevBuf* b : bufs) b->alloc(dN * C);
+        auto op = [&](const void* s, void* out) {  // kkt.py:274-289
+            apply_sym_c(k, g, s, out, SK_REG_KC);
+            rank_one(g, k->cdt, k->gmC.p, s, out, true, k->st);
+        };
+        auto pre = [&](const void* x, void* out) { apply_sym_c(k, g, x, out, SK_REG_INV); };
+        bool broke = inner_pcg(k, g, op, pre, r, k->c_x.p, k->c_r.p, k->c_z.p, k->c_s.p, k->c_q.p, tol, inner_max,
+                               &iters);
+        if (broke) {
+            k->precond_fallbacks += 1;
+            *fell_back = 1;
+            apply_sym_c(k, g, r, z, SK_REG_INV);
+            return;
+        }
+        FRG_CUDA(cudaMemcpyAsync(z, k->c_x.p, dN * C, cudaMemcpyDeviceToDevice, k->st));
+        return;
+    }
+    // two-level (kkt.py:325-341)
+    ensure_coarse(k);
+    Dims gc = coarse_dims(g);
+    const long long Nc = gc.N, dNc = (long long)gc.d * Nc;
+    k->c_w.alloc(dN * C);  // fine scratch: u
+    k->tmp2.alloc(dN * C);
+    DevBuf* cb[] = {&k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q};
+    for (DevBuf* b : cb) b->alloc(dN * C);
+    // c_q doubles as coarse rhs storage at the end of the fine buffers
+    void* u = k->c_w.p;
+    apply_sym_c(k, g, r, u, SK_REG_INV_SQRT);
+    apply_sym_c(k, g, u, k->tmp2.p, SK_LOWPASS);  // low band of u
+    k->tmp1.alloc(std::max((size_t)k->N() * k->T(), (size_t)dNc * C));
+    DevBuf rhs_c;
+    rhs_c.alloc(dNc * C);
+    void* rsws = k->ws_c.get(std::max(restrict_ws_bytes(g, k->cdt), spectral_ws_bytes(g, k->cdt, g.d)));
+    for (int c = 0; c < g.d; ++c)
+        restrict_field_ex(k->plans, rsws, g, k->cdt, (char*)k->tmp2.p + (size_t)c * g.N * C,
+                          (char*)rhs_c.p + (size_t)c * Nc * C, k->st);
+    // coarse operator: w + S[(g_c . S w) g_c],  S = (alpha L)^-1/2 on the coarse grid (kkt.py:298-306)
+    DevBuf tmpc;
+    tmpc.alloc(dNc * C);
+    auto op = [&](const void* w, void* out) {
+        apply_sym_c(k, gc, w, tmpc.p, SK_REG_INV_SQRT);
+        rank_one(gc, k->cdt, k->c_gm.p, tmpc.p, tmpc.p, false, k->st);
+        apply_sym_c(k, gc, tmpc.p, out, SK_REG_INV_SQRT);
+        axpby(k->cdt, 1.0, w, 1.0, out, dNc, k->st);
+    };
+    auto pre = [&](const void* x, void* out) {
+        FRG_CUDA(cudaMemcpyAsync(out, x, dNc * C, cudaMemcpyDeviceToDevice, k->st));
+    };
+    bool broke = inner_pcg(k, gc, op, pre, rhs_c.p, k->c_x.p, k->c_r.p, k->c_z.p, k->c_s.p, k->c_q.p, tol, inner_max,
+                           &iters);
+    if (broke) {
+        rhs_c.free_();
+        tmpc.free_();
+        k->precond_fallbacks += 1;
+        *fell_back = 1;
+        apply_sym_c(k, g, r, z, SK_REG_INV);
+        return;
+    }
+    // s = low_pass(prolong(sol)) + high_pass(u); z = S s
+    rsws = k->ws_c.get(std::max(restrict_ws_bytes(g, k->cdt), spectral_ws_bytes(g, k->cdt, g.d)));
+    for (int c = 0; c < g.d; ++c)
+        prolong_field_ex(k->plans, rsws, g, k->cdt, (char*)k->c_x.p + (size_t)c * Nc * C,
+                         (char*)k->tmp2.p + (size_t)c * g.N * C, k->st);
+    apply_sym_c(k, g, k->tmp2.p, k->tmp2.p, SK_LOWPASS);
+    apply_sym_c(k, g, u, z, SK_HIGHPASS);
+    axpby(k->cdt, 1.0, k->tmp2.p, 1.0, z, dN, k->st);
+    apply_sym_c(k, g, z, z, SK_REG_INV_SQRT);
+    rhs_c.free_();
+    tmpc.free_();
+}
+
+void kkt_counters(KktCtx* k, long long out[3]) {
+    out[0] = k->matvecs;
+    out[1] = k->pde_solves;
+    out[2] = k->precond_fallbacks;
+}
+
+void kkt_set_counters(KktCtx* k, const long long in[3]) {
+    k->matvecs = in[0];
+    k->pde_solves = in[1];
+    k->precond_fallbacks = in[2];
+}
+
+void kkt_get(KktCtx* k, int which, void* dst) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    const long long N = k->N(), d = k->g.d;
+    const size_t T = k->T();
+    const void* src = nullptr;
+    size_t bytes = 0;
+    switch (which) {
+        case 0: src = k->mseries.p; bytes = (k->n_t + 1) * N * T; break;
+        case 1: src = k->lam.p; bytes = (k->n_t + 1) * N * T; break;
+        case 2: src = k->disp_f.p; bytes = d * N * T; break;
+        case 3: src = k->disp_b.p; bytes = d * N * T; break;
+        case 4: src = k->divv.p; bytes = N * T; break;
+        case 5: src = k->grads.p; bytes = (k->n_t + 1) * d * N * T; break;
+        default: throw Error(E_ARG, "unknown series selector");
+    }
+    FRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, k->st));
+}
+
+// optimizer.py:169-171 (solve_deformation_tensor + determinant stats)
+void kkt_detgrad(KktCtx* k, double out[3]) {
+    FRG_REQUIRE(k->have_state, "refresh first");
+    const long long N = k->N(), d = k->g.d;
+    const size_t T = k->T();
+    DevBuf jac, F, work, det;
+    jac.alloc(d * d * N * T);
+    F.alloc(d * d * N * T);
+    work.alloc(2 * d * d * N * T);
+    det.alloc(N * T);
+    // jacobian rows = gradient of each velocity component (diffops.py:132-139)
+    gradient_slices(k, (int)d, k->vT.p, jac.p);
+    deformation_tensor(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, jac.p, F.p, work.p, k->st);
+    determinant(k->g, k->tdt, F.p, det.p, k->st);
+    double mms[3];
+    min_max_sum(k->tdt, det.p, N, mms, k->st);
+    out[0] = mms[0];
+    out[1] = mms[2] / (double)N;
+    out[2] = mms[1];
+    jac.free_();
+    F.free_();
+    work.free_();
+    det.free_();
+}
+
+}  // namespace frg

@@ -1,0 +1,632 @@
+// Spectral operators: cuFFT R2C/C2R (D2Z/Z2D) bracketed by fused pointwise
+// kernels on the half spectrum (diffops.py:44-366).
+//
+// The reference uses complex fftn/ifftn(...).real; every multiplier it
+// applies is Hermitian (real even symbols, -i m with the Nyquist bin zeroed,
+// the Nyquist-zeroed projection), so the real-to-complex pair computes the
+// same result with half the traffic.  Normalisation 1/N is folded into the
+// pointwise kernel.  Half-spectrum index (i0, i1, i2), i2 in [0, n2/2].
+#include <cufft.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "ops.h"
+#include "spectral.h"
+
+namespace frg {
+
+#define FRG_CUFFT(call)                                                                   \
+    do {                                                                                  \
+        cufftResult _r = (call);                                                          \
+        if (_r != CUFFT_SUCCESS)                                                          \
+            throw ::frg::Error(::frg::E_CUFFT, std::string(#call) + " failed: " + std::to_string((int)_r)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// plan cache
+// ---------------------------------------------------------------------------
+cufftHandle PlanCache::get(const Dims& g, int type, int batch) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(g.n0, g.n1, g.n2, type, batch);
+    auto it = plans.find(key);
+    if (it != plans.end()) return it->second;
+    cufftHandle h;
+    int dims3[3] = {g.n0, g.n1, g.n2};
+    int dims2[2] = {g.n1, g.n2};
+    int rank = g.n0 == 1 ? 2 : 3;
+    int* dims = rank == 3 ? dims3 : dims2;
+    FRG_CUFFT(cufftPlanMany(&h, rank, dims, nullptr, 1, 0, nullptr, 1, 0, (cufftType)type, batch));
+    plans[key] = h;
+    return h;
+}
+
+void PlanCache::clear() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : plans) cufftDestroy(kv.second);
+    plans.clear();
+}
+
+PlanCache::~PlanCache() {
+    // plans are intentionally leaked at process exit (the CUDA context may be gone)
+}
+
+static PlanCache g_plans;
+
+Workspace::~Workspace() {}
+void* Workspace::get(size_t bytes) {
+    if (bytes > cap) {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        FRG_CUDA(cudaMalloc(&ptr, bytes));
+        cap = bytes;
+    }
+    return ptr;
+}
+void Workspace::release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+}
+
+static Workspace g_ws;
+static std::mutex g_ws_mu;
+
+void spectral_release_plans() {
+    g_plans.clear();
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    g_ws.release();
+}
+
+long long half_len(const Dims& g) { return (long long)g.n0 * g.n1 * (g.n2 / 2 + 1); }
+
+template <typename R>
+struct CT;
+template <>
+struct CT<float> {
+    using C = cufftComplex;
+    static constexpr int R2C = CUFFT_R2C, C2R = CUFFT_C2R;
+};
+template <>
+struct CT<double> {
+    using C = cufftDoubleComplex;
+    static constexpr int R2C = CUFFT_D2Z, C2R = CUFFT_Z2D;
+};
+
+template <typename R>
+void fwd(PlanCache& pc, const Dims& g, int batch, const R* in, typename CT<R>::C* out, cudaStream_t st) {
+    cufftHandle h = pc.get(g, CT<R>::R2C, batch);
+    FRG_CUFFT(cufftSetStream(h, st));
+    if (sizeof(R) == 8)
+        FRG_CUFFT(cufftExecD2Z(h, (cufftDoubleReal*)in, (cufftDoubleComplex*)out));
+    else
+        FRG_CUFFT(cufftExecR2C(h, (cufftReal*)in, (cufftComplex*)out));
+}
+
+template <typename R>
+void inv(PlanCache& pc, const Dims& g, int batch, typename CT<R>::C* in, R* out, cudaStream_t st) {
+    cufftHandle h = pc.get(g, CT<R>::C2R, batch);
+    FRG_CUFFT(cufftSetStream(h, st));
+    if (sizeof(R) == 8)
+        FRG_CUFFT(cufftExecZ2D(h, (cufftDoubleComplex*)in, (cufftDoubleReal*)out));
+    else
+        FRG_CUFFT(cufftExecC2R(h, (cufftComplex*)in, (cufftReal*)out));
+}
+
+template void fwd<float>(PlanCache&, const Dims&, int, const float*, cufftComplex*, cudaStream_t);
+template void fwd<double>(PlanCache&, const Dims&, int, const double*, cufftDoubleComplex*, cudaStream_t);
+template void inv<float>(PlanCache&, const Dims&, int, cufftComplex*, float*, cudaStream_t);
+template void inv<double>(PlanCache&, const Dims&, int, cufftDoubleComplex*, double*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// symbols
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int dft_freq(int i, int n) { return i < (n + 1) / 2 ? i : i - n; }
+
+struct Bin {
+    double m[3];  // integer frequencies per axis (numpy fftfreq convention)
+    bool nyq[3];  // |m| == n/2 (for n > 1)
+};
+
+__device__ __forceinline__ Bin bin_of(const Dims& g, long long p) {
+    int nh = g.n2 / 2 + 1;
+    int i2 = (int)(p % nh);
+    long long r = p / nh;
+    int i1 = (int)(r % g.n1);
+    int i0 = (int)(r / g.n1);
+    Bin b;
+    int f0 = dft_freq(i0, g.n0), f1 = dft_freq(i1, g.n1);
+    int f2 = (i2 == g.n2 / 2) ? -(g.n2 / 2) : i2;
+    b.m[0] = f0;
+    b.m[1] = f1;
+    b.m[2] = f2;
+    b.nyq[0] = g.n0 > 1 && (f0 == -(g.n0 / 2));
+    b.nyq[1] = g.n1 > 1 && (f1 == -(g.n1 / 2));
+    b.nyq[2] = g.n2 > 1 && (i2 == g.n2 / 2);
+    return b;
+}
+
+__device__ __forceinline__ double ipow(double x, int o) {
+    double r = x;
+    for (int i = 1; i < o; ++i) r *= x;
+    return r;
+}
+
+// diffops.py:167-173
+__device__ __forceinline__ double reg_sym(double ksq, const RegSpec& r) {
+    return r.seminorm ? ipow(ksq, r.order) : ipow(1.0 + ksq, r.order);
+}
+
+__device__ __forceinline__ double symbol_of(const Dims& g, const Bin& b, int kind, const RegSpec& r) {
+    double ksq = b.m[0] * b.m[0] + b.m[1] * b.m[1] + b.m[2] * b.m[2];
+    switch (kind) {
+        case SK_REG: return r.alpha * reg_sym(ksq, r);
+        case SK_REG_INV: {
+            double s = reg_sym(ksq, r);
+            if (s == 0.0) s = 1.0;
+            return 1.0 / (r.alpha * s);
+        }
+        case SK_REG_INV_SQRT: {
+            double s = reg_sym(ksq, r);
+            if (s == 0.0) s = 1.0;
+            return 1.0 / sqrt(r.alpha * s);
+        }
+        case SK_REG_KC: {
+            double s = reg_sym(ksq, r);
+            if (s == 0.0) s = 1.0;
+            return r.alpha * s;
+        }
+        case SK_LAPLACIAN: return -ksq;
+        case SK_LOWPASS:
+        case SK_HIGHPASS: {
+            // diffops.py:283-289 — keep |k_i| < n_i / 4 on every axis
+            bool low = fabs(b.m[0]) < g.n0 / 4.0 && fabs(b.m[1]) < g.n1 / 4.0 && fabs(b.m[2]) < g.n2 / 4.0;
+            if (g.n0 == 1) low = fabs(b.m[1]) < g.n1 / 4.0 && fabs(b.m[2]) < g.n2 / 4.0;
+            return (kind == SK_LOWPASS) == low ? 1.0 : 0.0;
+        }
+    }
+    return 0.0;
+}
+
+// diffops.py:222-242, 245-280: factor M(k)/|k|^2 with Nyquist-zeroed k
+__device__ __forceinline__ void proj_k(const Dims& g, const Bin& b, const RegSpec& r, double k[3], double& mfac) {
+    for (int a = 0; a < 3; ++a) k[a] = b.nyq[a] ? 0.0 : b.m[a];
+    double ksq = k[0] * k[0] + k[1] * k[1] + k[2] * k[2];
+    if (ksq == 0.0 || r.incomp == 0) {
+        mfac = 0.0;
+        return;
+    }
+    double mult;
+    if (r.incomp == 1) {
+        mult = 1.0;
+    } else {
+        double inner = r.beta * (1.0 / ksq + 1.0);
+        mult = 1.0 / (r.alpha / inner + 1.0);
+    }
+    mfac = mult / ksq;
+}
+
+template <typename C>
+struct CR;
+template <>
+struct CR<cufftComplex> {
+    using R = float;
+};
+template <>
+struct CR<cufftDoubleComplex> {
+    using R = double;
+};
+
+template <typename C>
+__global__ void k_spec_scale(Dims g, long long nh, int ncomp, C* __restrict__ x, int kind, RegSpec r, double invN) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nh) return;
+    Bin b = bin_of(g, p);
+    double s = symbol_of(g, b, kind, r) * invN;
+    using R = typename CR<C>::R;
+    for (int c = 0; c < ncomp; ++c) {
+        C v = x[(long long)c * nh + p];
+        v.x = (R)(v.x * s);
+        v.y = (R)(v.y * s);
+        x[(long long)c * nh + p] = v;
+    }
+}
+
+// out = alpha sym a + P(b), both normalised; written into a's spectrum.
+// a may be null (P(b) only, written into b's spectrum converted to A).
+template <typename CA, typename CB>
+__global__ void k_spec_combine(Dims g, long long nh, CA* __restrict__ a, const CB* __restrict__ bsp, RegSpec r,
+                               double invN, bool have_a, bool project) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nh) return;
+    Bin bn = bin_of(g, p);
+    double ksq = bn.m[0] * bn.m[0] + bn.m[1] * bn.m[1] + bn.m[2] * bn.m[2];
+    double sa = have_a ? r.alpha * reg_sym(ksq, r) * invN : 0.0;
+    double br[3], bi[3], k[3] = {0, 0, 0}, mfac = 0.0;
+    for (int c = 0; c < g.d; ++c) {
+        CB v = bsp[(long long)c * nh + p];
+        br[c] = v.x;
+        bi[c] = v.y;
+    }
+    if (project) proj_k(g, bn, r, k, mfac);
+    double dr = 0.0, di = 0.0;
+    for (int c = 0; c < g.d; ++c) {
+        double kc = k[g.comp_axis(c)];
+        dr += kc * br[c];
+        di += kc * bi[c];
+    }
+    using RA = typename CR<CA>::R;
+    for (int c = 0; c < g.d; ++c) {
+        double kc = k[g.comp_axis(c)];
+        double orr = (br[c] - kc * mfac * dr) * invN;
+        double oi = (bi[c] - kc * mfac * di) * invN;
+        CA o;
+        if (have_a) {
+            CA av = a[(long long)c * nh + p];
+            orr += sa * av.x;
+            oi += sa * av.y;
+        }
+        o.x = (RA)orr;
+        o.y = (RA)oi;
+        a[(long long)c * nh + p] = o;
+    }
+}
+
+// spectral gradient of a scalar: out_c = -i m_axis(c) u  (Nyquist zeroed), diffops.py:56-73
+template <typename C>
+__global__ void k_spec_grad(Dims g, long long nh, const C* __restrict__ u, C* __restrict__ out, double invN) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nh) return;
+    Bin b = bin_of(g, p);
+    C v = u[p];
+    using R = typename CR<C>::R;
+    for (int c = 0; c < g.d; ++c) {
+        int a = g.comp_axis(c);
+        double m = b.nyq[a] ? 0.0 : b.m[a];
+        // (-i m)(x + i y) = m y - i m x
+        C o;
+        o.x = (R)(m * v.y * invN);
+        o.y = (R)(-m * v.x * invN);
+        out[(long long)c * nh + p] = o;
+    }
+}
+
+template <typename C>
+__global__ void k_spec_div(Dims g, long long nh, const C* __restrict__ v, C* __restrict__ out, double invN) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nh) return;
+    Bin b = bin_of(g, p);
+    double orr = 0.0, oi = 0.0;
+    for (int c = 0; c < g.d; ++c) {
+        int a = g.comp_axis(c);
+        double m = b.nyq[a] ? 0.0 : b.m[a];
+        C x = v[(long long)c * nh + p];
+        orr += m * x.y;
+        oi += -m * x.x;
+    }
+    using R = typename CR<C>::R;
+    C o;
+    o.x = (R)(orr * invN);
+    o.y = (R)(oi * invN);
+    out[p] = o;
+}
+
+// Parseval: per-bin weight (1 on the i2 = 0 and i2 = n2/2 planes, else 2)
+template <typename C>
+__global__ void k_spec_energy(Dims g, long long nh, const C* __restrict__ v, RegSpec r, double* __restrict__ out) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nh) return;
+    Bin b = bin_of(g, p);
+    int nhz = g.n2 / 2 + 1;
+    int i2 = (int)(p % nhz);
+    double w = (i2 == 0 || i2 == g.n2 / 2) ? 1.0 : 2.0;
+    double ksq = b.m[0] * b.m[0] + b.m[1] * b.m[1] + b.m[2] * b.m[2];
+    double s = r.alpha * reg_sym(ksq, r);
+    double acc = 0.0;
+    for (int c = 0; c < g.d; ++c) {
+        C x = v[(long long)c * nh + p];
+        acc += (double)x.x * (double)x.x + (double)x.y * (double)x.y;
+    }
+    out[p] = w * s * acc;
+}
+
+// restriction: coarse spectrum from fine (diffops.py:304-326)
+__device__ __forceinline__ int coarse_to_fine_full(int j, int c, int n) {
+    // kept coarse bins: [0, c/2) and [c - c/2 + 1, c); the coarse Nyquist c/2 is dropped
+    if (n == 1) return 0;
+    if (j < c / 2) return j;
+    if (j >= c - c / 2 + 1) return j + (n - c);
+    return -1;
+}
+
+template <typename C>
+__global__ void k_restrict_spec(Dims gf, Dims gc, const C* __restrict__ fine, C* __restrict__ coarse, double scale) {
+    long long nhc = (long long)gc.n0 * gc.n1 * (gc.n2 / 2 + 1);
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nhc) return;
+    int nh_c = gc.n2 / 2 + 1, nh_f = gf.n2 / 2 + 1;
+    int j2 = (int)(p % nh_c);
+    long long r = p / nh_c;
+    int j1 = (int)(r % gc.n1);
+    int j0 = (int)(r / gc.n1);
+    int f0 = coarse_to_fine_full(j0, gc.n0, gf.n0);
+    int f1 = coarse_to_fine_full(j1, gc.n1, gf.n1);
+    int f2 = j2 < gc.n2 / 2 ? j2 : -1;
+    C o;
+    o.x = 0;
+    o.y = 0;
+    if (f0 >= 0 && f1 >= 0 && f2 >= 0) {
+        C v = fine[((long long)f0 * gf.n1 + f1) * nh_f + f2];
+        o.x = (typename CR<C>::R)(v.x * scale);
+        o.y = (typename CR<C>::R)(v.y * scale);
+    }
+    coarse[p] = o;
+}
+
+__device__ __forceinline__ int fine_to_coarse_full(int f, int c, int n) {
+    if (n == 1) return 0;
+    if (f < c / 2) return f;
+    if (f >= n - c / 2 + 1) return f - (n - c);
+    return -1;
+}
+
+template <typename C>
+__global__ void k_prolong_spec(Dims gf, Dims gc, const C* __restrict__ coarse, C* __restrict__ fine, double scale) {
+    long long nhf = (long long)gf.n0 * gf.n1 * (gf.n2 / 2 + 1);
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nhf) return;
+    int nh_c = gc.n2 / 2 + 1, nh_f = gf.n2 / 2 + 1;
+    int f2 = (int)(p % nh_f);
+    long long r = p / nh_f;
+    int f1 = (int)(r % gf.n1);
+    int f0 = (int)(r / gf.n1);
+    int j0 = fine_to_coarse_full(f0, gc.n0, gf.n0);
+    int j1 = fine_to_coarse_full(f1, gc.n1, gf.n1);
+    int j2 = f2 < gc.n2 / 2 ? f2 : -1;
+    C o;
+    o.x = 0;
+    o.y = 0;
+    if (j0 >= 0 && j1 >= 0 && j2 >= 0) {
+        C v = coarse[((long long)j0 * gc.n1 + j1) * nh_c + j2];
+        o.x = (typename CR<C>::R)(v.x * scale);
+        o.y = (typename CR<C>::R)(v.y * scale);
+    }
+    fine[p] = o;
+}
+
+// ---------------------------------------------------------------------------
+// host entry points
+// ---------------------------------------------------------------------------
+constexpr int S_TPB = 256;
+
+template <typename R>
+static void spectral_apply_t(PlanCache& pc, void* ws, const Dims& g, int ncomp, const R* in, R* out, int kind,
+                             const RegSpec& r, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    long long nh = half_len(g);
+    C* sp = (C*)ws;
+    fwd<R>(pc, g, ncomp, in, sp, st);
+    k_spec_scale<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ncomp, sp, kind, r, 1.0 / (double)g.N);
+    FRG_CHECK_LAUNCH();
+    inv<R>(pc, g, ncomp, sp, out, st);
+}
+
+size_t spectral_ws_bytes(const Dims& g, int dtype, int ncomp) {
+    return (size_t)half_len(g) * (dtype == F64 ? 16 : 8) * ncomp + (size_t)half_len(g) * 8;
+}
+
+void spectral_apply_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, int ncomp, const void* in, void* out,
+                       int kind, const RegSpec& r, cudaStream_t st) {
+    if (dtype == F64)
+        spectral_apply_t<double>(pc, ws, g, ncomp, (const double*)in, (double*)out, kind, r, st);
+    else
+        spectral_apply_t<float>(pc, ws, g, ncomp, (const float*)in, (float*)out, kind, r, st);
+}
+
+void spectral_apply(const Dims& g, int dtype, int ncomp, const void* in, void* out, int kind, const RegSpec& r,
+                    cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    void* ws = g_ws.get(spectral_ws_bytes(g, dtype, ncomp));
+    spectral_apply_ex(g_plans, ws, g, dtype, ncomp, in, out, kind, r, st);
+}
+
+template <typename RA, typename RB>
+static void combine_t(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const RA* a, const RB* b, RA* out,
+                      const RegSpec& r, bool project_on, cudaStream_t st) {
+    using CA = typename CT<RA>::C;
+    using CB = typename CT<RB>::C;
+    long long nh = half_len(g);
+    CA* sa = (CA*)ws_a;
+    CB* sb = (CB*)ws_b;
+    if (a) fwd<RA>(pc, g, g.d, a, sa, st);
+    fwd<RB>(pc, g, g.d, b, sb, st);
+    k_spec_combine<CA, CB><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, sa, sb, r, 1.0 / (double)g.N, a != nullptr,
+                                                                     project_on);
+    FRG_CHECK_LAUNCH();
+    inv<RA>(pc, g, g.d, sa, out, st);
+}
+
+void reg_plus_project_ex(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, int adtype, const void* a,
+                         int bdtype, const void* b, void* out, const RegSpec& r, bool project_on, cudaStream_t st) {
+    if (adtype == F64 && bdtype == F64)
+        combine_t<double, double>(pc, ws_a, ws_b, g, (const double*)a, (const double*)b, (double*)out, r, project_on, st);
+    else if (adtype == F32 && bdtype == F32)
+        combine_t<float, float>(pc, ws_a, ws_b, g, (const float*)a, (const float*)b, (float*)out, r, project_on, st);
+    else if (adtype == F64 && bdtype == F32)
+        combine_t<double, float>(pc, ws_a, ws_b, g, (const double*)a, (const float*)b, (double*)out, r, project_on, st);
+    else
+        throw Error(E_ARG, "reg_plus_project: unsupported dtypes");
+}
+
+void reg_plus_project(const Dims& g, int adtype, const void* a, int bdtype, const void* b, void* out,
+                      const RegSpec& r, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    size_t sa = (size_t)half_len(g) * (adtype == F64 ? 16 : 8) * g.d;
+    size_t sb = (size_t)half_len(g) * (bdtype == F64 ? 16 : 8) * g.d;
+    char* ws = (char*)g_ws.get(sa + sb);
+    reg_plus_project_ex(g_plans, ws, ws + sa, g, adtype, a, bdtype, b, out, r, true, st);
+}
+
+void project(const Dims& g, int dtype, const void* b, void* out, const RegSpec& r, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    size_t sb = (size_t)half_len(g) * (dtype == F64 ? 16 : 8) * g.d;
+    char* ws = (char*)g_ws.get(sb);
+    // P(b) only: the combine kernel writes into the "a" spectrum -> use the same buffer
+    if (dtype == F64) {
+        using C = cufftDoubleComplex;
+        long long nh = half_len(g);
+        fwd<double>(g_plans, g, g.d, (const double*)b, (C*)ws, st);
+        k_spec_combine<C, C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
+                                                                       1.0 / (double)g.N, false, true);
+        FRG_CHECK_LAUNCH();
+        inv<double>(g_plans, g, g.d, (C*)ws, (double*)out, st);
+    } else {
+        using C = cufftComplex;
+        long long nh = half_len(g);
+        fwd<float>(g_plans, g, g.d, (const float*)b, (C*)ws, st);
+        k_spec_combine<C, C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
+                                                                       1.0 / (double)g.N, false, true);
+        FRG_CHECK_LAUNCH();
+        inv<float>(g_plans, g, g.d, (C*)ws, (float*)out, st);
+    }
+}
+
+template <typename R>
+static void spec_grad_t(const Dims& g, const R* u, R* out, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    long long nh = half_len(g);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    C* ws = (C*)g_ws.get(sizeof(C) * nh * (g.d + 1));
+    fwd<R>(g_plans, g, 1, u, ws, st);
+    k_spec_grad<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, ws + nh, 1.0 / (double)g.N);
+    FRG_CHECK_LAUNCH();
+    inv<R>(g_plans, g, g.d, ws + nh, out, st);
+}
+
+void spectral_gradient(const Dims& g, int dtype, const void* u, void* out, cudaStream_t st) {
+    if (dtype == F64)
+        spec_grad_t<double>(g, (const double*)u, (double*)out, st);
+    else
+        spec_grad_t<float>(g, (const float*)u, (float*)out, st);
+}
+
+template <typename R>
+static void spec_div_t(const Dims& g, const R* v, R* out, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    long long nh = half_len(g);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    C* ws = (C*)g_ws.get(sizeof(C) * nh * (g.d + 1));
+    fwd<R>(g_plans, g, g.d, v, ws, st);
+    k_spec_div<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, ws + (long long)g.d * nh, 1.0 / (double)g.N);
+    FRG_CHECK_LAUNCH();
+    inv<R>(g_plans, g, 1, ws + (long long)g.d * nh, out, st);
+}
+
+void spectral_divergence(const Dims& g, int dtype, const void* v, void* out, cudaStream_t st) {
+    if (dtype == F64)
+        spec_div_t<double>(g, (const double*)v, (double*)out, st);
+    else
+        spec_div_t<float>(g, (const float*)v, (float*)out, st);
+}
+
+template <typename R>
+static double reg_energy_t(PlanCache& pc, void* wsv, const Dims& g, const R* v, const RegSpec& r, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    long long nh = half_len(g);
+    C* ws = (C*)wsv;
+    double* vals = (double*)(ws + (long long)g.d * nh);
+    fwd<R>(pc, g, g.d, v, ws, st);
+    k_spec_energy<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, r, vals);
+    FRG_CHECK_LAUNCH();
+    double mms[3];
+    min_max_sum(F64, vals, nh, mms, st);
+    double cellvol = (TWO_PI / g.n0) * (TWO_PI / g.n1) * (TWO_PI / g.n2);
+    if (g.n0 == 1) cellvol = (TWO_PI / g.n1) * (TWO_PI / g.n2);
+    // sum_x (aLv) v = (1/N) sum_k a sym |v^|^2
+    return 0.5 * mms[2] / (double)g.N * cellvol;
+}
+
+double reg_energy_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, const void* v, const RegSpec& r,
+                     cudaStream_t st) {
+    if (dtype == F64) return reg_energy_t<double>(pc, ws, g, (const double*)v, r, st);
+    return reg_energy_t<float>(pc, ws, g, (const float*)v, r, st);
+}
+
+double reg_energy(const Dims& g, int dtype, const void* v, const RegSpec& r, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    void* ws = g_ws.get(spectral_ws_bytes(g, dtype, g.d));
+    return reg_energy_ex(g_plans, ws, g, dtype, v, r, st);
+}
+
+Dims coarse_dims(const Dims& gf) {
+    Dims gc = gf;
+    gc.n0 = gf.n0 == 1 ? 1 : gf.n0 / 2;
+    gc.n1 = gf.n1 / 2;
+    gc.n2 = gf.n2 / 2;
+    gc.N = (long long)gc.n0 * gc.n1 * gc.n2;
+    return gc;
+}
+
+template <typename R>
+static void restrict_t(PlanCache& pc, void* wsv, const Dims& gf, const R* in, R* out, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    Dims gc = coarse_dims(gf);
+    long long nhf = half_len(gf), nhc = half_len(gc);
+    C* wf = (C*)wsv;
+    C* wc = wf + nhf;
+    fwd<R>(pc, gf, 1, in, wf, st);
+    // (Nc/Nf) amplitude scale times the 1/Nc of the coarse inverse
+    k_restrict_spec<C><<<blocks_for(nhc, S_TPB), S_TPB, 0, st>>>(gf, gc, wf, wc, 1.0 / (double)gf.N);
+    FRG_CHECK_LAUNCH();
+    inv<R>(pc, gc, 1, wc, out, st);
+}
+
+template <typename R>
+static void prolong_t(PlanCache& pc, void* wsv, const Dims& gf, const R* in, R* out, cudaStream_t st) {
+    using C = typename CT<R>::C;
+    Dims gc = coarse_dims(gf);
+    long long nhf = half_len(gf), nhc = half_len(gc);
+    C* wf = (C*)wsv;
+    C* wc = wf + nhf;
+    fwd<R>(pc, gc, 1, in, wc, st);
+    // (Nf/Nc) amplitude scale times the 1/Nf of the fine inverse
+    k_prolong_spec<C><<<blocks_for(nhf, S_TPB), S_TPB, 0, st>>>(gf, gc, wc, wf, 1.0 / (double)gc.N);
+    FRG_CHECK_LAUNCH();
+    inv<R>(pc, gf, 1, wf, out, st);
+}
+
+size_t restrict_ws_bytes(const Dims& gf, int dtype) {
+    Dims gc = coarse_dims(gf);
+    return (size_t)(half_len(gf) + half_len(gc)) * (dtype == F64 ? 16 : 8);
+}
+
+void restrict_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st) {
+    if (dtype == F64)
+        restrict_t<double>(pc, ws, gf, (const double*)in, (double*)out, st);
+    else
+        restrict_t<float>(pc, ws, gf, (const float*)in, (float*)out, st);
+}
+
+void prolong_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st) {
+    if (dtype == F64)
+        prolong_t<double>(pc, ws, gf, (const double*)in, (double*)out, st);
+    else
+        prolong_t<float>(pc, ws, gf, (const float*)in, (float*)out, st);
+}
+
+void restrict_field(const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st) {
+    FRG_REQUIRE((gf.n0 == 1 || gf.n0 % 4 == 0) && gf.n1 % 4 == 0 && gf.n2 % 4 == 0,
+                "coarsening requires n_i divisible by 4");
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    void* ws = g_ws.get(restrict_ws_bytes(gf, dtype));
+    restrict_field_ex(g_plans, ws, gf, dtype, in, out, st);
+}
+
+void prolong_field(const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    void* ws = g_ws.get(restrict_ws_bytes(gf, dtype));
+    prolong_field_ex(g_plans, ws, gf, dtype, in, out, st);
+}
+
+}  // namespace frg

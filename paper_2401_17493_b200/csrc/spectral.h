@@ -1,0 +1,44 @@
+// cuFFT plan cache / workspace shared by spectral.cu and kkt.cu.
+#pragma once
+
+#include <cufft.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "ops.h"
+
+namespace frg {
+
+struct PlanCache {
+    std::map<std::tuple<int, int, int, int, int>, cufftHandle> plans;
+    std::mutex mu;
+    cufftHandle get(const Dims& g, int type, int batch);
+    void clear();
+    ~PlanCache();
+};
+
+struct Workspace {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes);
+    void release();
+    ~Workspace();
+};
+
+long long half_len(const Dims& g);
+Dims coarse_dims(const Dims& gf);
+size_t spectral_ws_bytes(const Dims& g, int dtype, int ncomp);
+size_t restrict_ws_bytes(const Dims& gf, int dtype);
+void spectral_apply_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, int ncomp, const void* in, void* out,
+                       int kind, const RegSpec& r, cudaStream_t st);
+// out = alpha L a + P[b] (project_on) or alpha L a + b; ws_a/ws_b hold d half spectra each
+void reg_plus_project_ex(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, int adtype, const void* a,
+                         int bdtype, const void* b, void* out, const RegSpec& r, bool project_on, cudaStream_t st);
+double reg_energy_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, const void* v, const RegSpec& r,
+                     cudaStream_t st);
+void restrict_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
+void prolong_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
+
+}  // namespace frg

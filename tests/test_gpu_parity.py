@@ -1,0 +1,308 @@
+"""CUDA path vs the reference's own outputs (golden fixtures) and the oracle.
+
+Tolerances (north star, BASELINE.json): f64 path within 1e-10 relative of
+the f64 reference (cuFFT vs pocketfft and FMA contraction are the only
+differences); fp32 transport within relative L2 1e-5 of the f64 reference.
+"""
+import numpy as np
+import pytest
+
+import inputs as I
+from conftest import max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2401_17493_b200 as F  # noqa: E402
+from paper_2401_17493_b200 import diffops, transport  # noqa: E402
+from paper_2401_17493_b200._kernels import sample_nd  # noqa: E402
+from paper_2401_17493_b200.fields import Grid, ScalarField, VectorField  # noqa: E402
+from paper_2401_17493_b200.kkt import KktState, PrecondKind, RegConfig  # noqa: E402
+
+F64_TOL = 1e-10
+F32_L2 = 1e-5
+
+
+def np_(x):
+    if hasattr(x, "values") and not hasattr(x, "data"):
+        x = x.values
+    elif hasattr(x, "data") and not isinstance(x, (np.ndarray, torch.Tensor)):
+        x = x.data
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+# ---------------------------------------------------------------------------
+# a1: sample_nd (narrow boundary)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", I.SAMPLE_SHAPES)
+def test_sample_nd_matches_reference(golden, shape):
+    g = golden("sample.npz")
+    rng = np.random.default_rng(I.SEED)
+    for s in I.SAMPLE_SHAPES:
+        vals, q, labels = I.sample_inputs(s, rng)
+        if s == shape:
+            break
+    t = f"{len(shape)}d"
+    qs = [q[i] for i in range(len(shape))]
+    for method in ("nearest", "linear", "cubic"):
+        out = sample_nd(vals, qs, method)
+        assert out.dtype == np.float64
+        ref = g[f"{t}_{method}_f64"]
+        if method == "nearest":
+            assert np.array_equal(out, ref)
+        else:
+            assert np.max(np.abs(out - ref)) < 1e-13, method
+        out32 = sample_nd(vals.astype(np.float32), qs, method)
+        assert out32.dtype == np.float32
+        ref32 = g[f"{t}_{method}_f32"]
+        # f64 accumulate then round: at most one f32 ulp from the reference
+        assert np.max(np.abs(out32 - ref32) / np.maximum(np.abs(ref32), 1e-30)) < 2e-7, method
+    assert np.array_equal(sample_nd(labels, qs, "nearest"), g[f"{t}_nearest_i32"])
+
+
+def test_sample_nd_unknown_method():
+    with pytest.raises(ValueError):
+        sample_nd(np.zeros((8, 8)), [np.zeros(2), np.zeros(2)], "quintic")
+
+
+def test_sample_nd_empty_and_device_inputs():
+    vals = torch.randn(10, 12, 14, dtype=torch.float64, device="cuda")
+    e = torch.zeros(0, dtype=torch.float64, device="cuda")
+    assert sample_nd(vals, [e, e, e], "cubic").numel() == 0
+    q = [torch.full((5,), 3.0, dtype=torch.float64, device="cuda")] * 3
+    out = sample_nd(vals, q, "cubic")
+    assert out.is_cuda and torch.allclose(out, vals[3, 3, 3].expand(5), atol=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# a6, a10-a12: differential operators
+# ---------------------------------------------------------------------------
+def _diff_inputs():
+    rng = np.random.default_rng(I.SEED + 1)
+    ins = {}
+    for shape in I.DIFFOPS_SHAPES:
+        ins[shape] = I.diffops_inputs(shape, rng)
+    for shape in I.FILTER_SHAPES:
+        ins[("f",) + shape] = I.filter_inputs(shape, rng)
+    return ins
+
+
+@pytest.mark.parametrize("shape", I.DIFFOPS_SHAPES)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_diffops_match_reference(golden, shape, dtype):
+    g = golden("diffops.npz")
+    u, v = _diff_inputs()[shape]
+    t = f"{len(shape)}d"
+    grid = Grid(shape, dtype=dtype)
+    U, V = ScalarField(grid, u), VectorField(grid, v)
+
+    def ok(a, ref):
+        a = np_(a)
+        if dtype == np.float64:
+            return max_rel(a, ref) < F64_TOL
+        return rel_l2(a, ref) < F32_L2
+
+    assert ok(diffops.fd8_gradient(U), g[f"{t}_fd8_grad"])
+    assert ok(diffops.spectral_gradient(U), g[f"{t}_spec_grad"])
+    assert ok(diffops.divergence(V, "fd8"), g[f"{t}_div_fd8"])
+    assert ok(diffops.divergence(V, "spectral"), g[f"{t}_div_spec"])
+    assert ok(diffops.jacobian(V, "fd8"), g[f"{t}_jacobian"])
+    assert ok(diffops.laplacian(U), g[f"{t}_laplacian"])
+    for order, semi in I.REG_VARIANTS:
+        k = f"{t}_o{order}{'s' if semi else 'f'}"
+        spec = diffops.RegOperatorSpec(order, semi)
+        assert ok(diffops.apply_reg_operator(V, spec, 0.03), g[k + "_L"]), k
+        assert ok(diffops.apply_inv_reg_operator(V, spec, 0.03), g[k + "_Linv"]), k
+        assert ok(diffops.apply_inv_sqrt_reg_operator(V, spec, 0.03), g[k + "_Linvsqrt"]), k
+    assert ok(diffops.project_body_force(V, diffops.IncompressibilityMode("incompressible"), 0.01),
+              g[f"{t}_proj_incomp"])
+    assert ok(diffops.project_body_force(V, diffops.IncompressibilityMode("near-incompressible", 1e-4), 0.01),
+              g[f"{t}_proj_near"])
+
+
+@pytest.mark.parametrize("shape", I.FILTER_SHAPES)
+def test_filters_restrict_prolong(golden, shape):
+    g = golden("diffops.npz")
+    u, uc = _diff_inputs()[("f",) + shape]
+    t = f"{len(shape)}d"
+    grid = Grid(shape)
+    U = ScalarField(grid, u)
+    assert max_rel(np_(diffops.low_pass(U)), g[f"{t}_lowpass"]) < F64_TOL
+    assert max_rel(np_(diffops.high_pass(U)), g[f"{t}_highpass"]) < F64_TOL
+    assert max_rel(np_(diffops.restrict(U)), g[f"{t}_restrict"]) < F64_TOL
+    assert max_rel(np_(diffops.prolong(ScalarField(grid.coarsen(), uc), grid)), g[f"{t}_prolong"]) < F64_TOL
+
+
+# ---------------------------------------------------------------------------
+# a2-a7, a17: transport
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", I.TRANSPORT_SHAPES)
+@pytest.mark.parametrize("method", ["cubic", "linear"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_transport_matches_reference(golden, shape, method, dtype):
+    g = golden("transport.npz")
+    rng = np.random.default_rng(I.SEED + 2)
+    for s in I.TRANSPORT_SHAPES:
+        m0, v, vt, lam1 = I.transport_inputs(s, rng)
+        if s == shape:
+            break
+    k = f"{len(shape)}d_{method}"
+    grid = Grid(shape, n_t=4, dtype=dtype)
+    V = VectorField(grid, v)
+
+    def ok(a, ref, tol=F64_TOL):
+        a = np_(a)
+        if dtype == np.float64:
+            return max_rel(a, ref) < tol
+        return rel_l2(a, ref) < F32_L2
+
+    traj = transport.Trajectory.compute(V, method)
+    back = transport.Trajectory.compute(VectorField(grid, -v), method)
+    assert ok(traj.step_points, g[k + "_y"], 1e-13)
+    assert ok(back.step_points, g[k + "_yb"], 1e-13)
+    ms = transport.solve_state(ScalarField(grid, m0), V, method, traj)
+    assert ok(ms, g[k + "_state"])
+    adj = transport.solve_adjoint(ScalarField(grid, lam1), V, method, "fd8", back)
+    assert ok(adj, g[k + "_adjoint"])
+    inc = transport.solve_inc_state(ms, V, VectorField(grid, vt), method, "fd8", traj)
+    assert ok(inc.data[-1], g[k + "_incstate"])
+    Fd = transport.solve_deformation_tensor(V, method, "fd8", traj)
+    assert ok(Fd.determinant(), g[k + "_det"])
+    assert ok(Fd.data[0, 0], g[k + "_F00"])
+    assert ok(transport.compose_trajectory(V, method), g[k + "_composed"], 1e-12)
+
+
+def test_zero_velocity_transports_are_exact(rng):
+    """reference tests/test_transport.py:63-68,119-124 (array_equal at v = 0)."""
+    grid = Grid((16, 16), n_t=3)
+    m0 = ScalarField(grid, rng.standard_normal(grid.n))
+    out = transport.solve_state(m0, VectorField.zeros(grid))
+    for j in range(4):
+        assert torch.equal(out.data[j], m0.values)
+    lam = transport.solve_adjoint(m0, VectorField.zeros(grid))
+    for j in range(4):
+        assert torch.equal(lam.data[j], m0.values)
+
+
+# ---------------------------------------------------------------------------
+# a8-a15: KktState (wide boundary)
+# ---------------------------------------------------------------------------
+def _reg(regkw):
+    return RegConfig(alpha=1e-2, operator=diffops.RegOperatorSpec(regkw.get("order", 1), regkw.get("seminorm", True)),
+                     incomp=diffops.IncompressibilityMode(regkw.get("incomp", "none"), 1e-4))
+
+
+def _kkt_case(name):
+    rng = np.random.default_rng(I.SEED + 3)
+    for c in I.KKT_CASES:
+        ins = I.kkt_inputs(c[1], rng)
+        if c[0] == name:
+            return c, ins
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", [c[0] for c in I.KKT_CASES])
+@pytest.mark.parametrize("mode", ["f64", "mixed", "f32"])
+def test_kkt_matches_reference(golden, name, mode):
+    g = golden("kkt.npz")
+    meta = golden("kkt.json")[name]
+    (name, shape, regkw, dist, method, preconds), (m0, m1, v, vt, r) = _kkt_case(name)
+    dtype = np.float32 if mode == "f32" else np.float64
+    tdt = np.float32 if mode in ("mixed", "f32") else None
+    grid = Grid(shape, n_t=4, dtype=dtype)
+    st = KktState(ScalarField(grid, m0), ScalarField(grid, m1), _reg(regkw), distance=dist, method=method,
+                  scheme="fd8", v_init=VectorField(grid, v), transport_dtype=tdt)
+    p = name + "_"
+
+    def ok(a, ref, tol=F64_TOL):
+        a = np_(a)
+        if mode == "f64":
+            return max_rel(a, ref) < tol
+        return rel_l2(a, ref) < F32_L2
+
+    assert ok(st.mseries.data[-1], g[p + "m_final"])
+    assert ok(st.lamseries.data[0], g[p + "lam0"])
+    assert ok(st.gradient(), g[p + "gradient"])
+    assert ok(st.hessian_matvec(VectorField(grid, vt)), g[p + "matvec"])
+    for kind in preconds:
+        assert ok(st.apply_precond(VectorField(grid, r), PrecondKind(kind), 0.3), g[p + "precond_" + kind], 1e-9), kind
+    rt = 1e-10 if mode == "f64" else 1e-5
+    assert st.objective() == pytest.approx(meta["objective"], rel=rt)
+    assert st.objective_at(VectorField(grid, v + 0.1 * vt)) == pytest.approx(meta["objective_at"], rel=rt)
+    assert st.mismatch() == pytest.approx(meta["mismatch"], rel=rt)
+    assert st.divergence_energy() == pytest.approx(meta["divergence_energy"], rel=max(rt, 1e-9), abs=1e-300)
+    assert (st.matvecs, st.pde_solves, st.precond_fallbacks) == (meta["matvecs"], meta["pde_solves"],
+                                                                  meta["precond_fallbacks"])
+
+
+def test_matvec_rest_state_formula():
+    """reference tests/test_kkt.py:99-112: at v = 0, H v~ = aL v~ + (grad m0 . v~) grad m0."""
+    from oracle import flowreg_oracle as O
+
+    m0, m1, _ = O.synth_case("rotation", 32, seed=3, d=2)
+    grid = Grid((32, 32))
+    st = KktState(ScalarField(grid, m0), ScalarField(grid, m1), _reg({}))
+    rng = np.random.default_rng(7)
+    vt = I.smooth_vector(rng, grid.n, 0.6, kmax=2)
+    out = np_(st.hessian_matvec(VectorField(grid, vt)))
+    gm = O.fd8_grad(m0)
+    expected = O.reg_apply(vt, 1e-2) + np.sum(gm * vt, axis=0) * gm
+    assert np.max(np.abs(out - expected)) / np.max(np.abs(expected)) < 1e-12
+
+
+def test_gn_symmetry():
+    """reference tests/test_kkt.py:129-139."""
+    from oracle import flowreg_oracle as O
+
+    m0, m1, _ = O.synth_case("rotation", 64, seed=5, d=2)
+    grid = Grid((64, 64))
+    rng = np.random.default_rng(3)
+    st = KktState(ScalarField(grid, m0), ScalarField(grid, m1), _reg({}),
+                  v_init=VectorField(grid, I.smooth_vector(rng, grid.n, 0.3, kmax=2)))
+    for _ in range(3):
+        a = VectorField(grid, I.smooth_vector(rng, grid.n, 1.0))
+        b = VectorField(grid, I.smooth_vector(rng, grid.n, 1.0))
+        ha, hb = st.hessian_matvec(a), st.hessian_matvec(b)
+        rel = abs(F.l2_inner(ha, b) - F.l2_inner(a, hb)) / (F.norm_l2(ha) * F.norm_l2(b))
+        assert rel < 1e-3
+
+
+def test_nonfinite_and_grid_errors():
+    grid = Grid((16, 16))
+    bad = np.zeros(grid.n)
+    bad[3, 4] = np.nan
+    with pytest.raises(ValueError):
+        ScalarField(grid, bad)
+    with pytest.raises(ValueError):
+        RegConfig(alpha=0.0)
+    m = ScalarField(grid, np.ones(grid.n))
+    with pytest.raises(ValueError):
+        KktState(m, ScalarField(Grid((16, 18)), np.ones((16, 18))), _reg({}))
+
+
+# ---------------------------------------------------------------------------
+# a16, a18: optimizer / continuation end to end
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", [c[0] for c in I.REGISTER_CASES if c[5]])
+def test_register_matches_reference(golden, name):
+    meta = golden("register.json")[name]
+    gv = golden("register.npz")[name + "_v"]
+    case = next(c for c in I.REGISTER_CASES if c[0] == name)
+    _, (sc, n, seed, d), regkw, pre, method, _ = case
+    m0, m1, _ = F.synth_case(sc, n, seed=seed, d=d)
+    v, rep = F.register(m0, m1, reg=_reg(regkw), precond=PrecondKind(pre), method=method, scheme="fd8")
+    assert rep.status == meta["status"]
+    assert rep.exit_reason == meta["exit_reason"]
+    assert rep.iterations == meta["iterations"]
+    assert rep.matvecs == meta["matvecs"]
+    assert rep.pde_solves == meta["pde_solves"]
+    assert rep.line_search_evals == meta["line_search_evals"]
+    assert [t["pcg_iterations"] for t in rep.trace] == [t["pcg_iterations"] for t in meta["trace"]]
+    assert rep.mismatch == pytest.approx(meta["mismatch"], rel=1e-6)
+    assert rep.detgrad_min == pytest.approx(meta["detgrad_min"], rel=1e-6)
+    assert rel_l2(np_(v), gv) < 1e-5
