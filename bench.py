@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""Benchmark: Gauss-Newton Hessian matvecs/s at 256^3 (+ time-to-solution and
+interpolation GB/s vs the HBM roofline) — BASELINE.json metric, config C3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one ``KktState.hessian_matvec`` (kkt.py:237-260) at 256^3, d = 3,
+n_t = 4, cubic Lagrange SL, FD8, H1 seminorm, near-incompressible beta=1e-4,
+alpha = 1e-2, SSD, state fixed at v = v_true / 2 of synth_case("rotation",
+256, seed=1); v~ = 0.1 N(0, 1) (seed 0).  Transport in fp32, velocity-space
+vectors in fp64 (SURVEY.md §7 hard part 1).  Synthetic data generated on the
+device.  Every matvec touches several GB, far above the 126 MB L2, so no L2
+flush is needed between steps.
+
+Multi-GPU (torchrun, one rank per GPU): every rank solves its own 256^3
+problem (independent registrations, weak scaling, no data-path collective);
+the barrier + max-over-ranks timing uses NCCL.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port, oracle/flowreg_oracle.py: C/OpenMP gathers + pocketfft) on the
+host cores for the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Hessian matvecs/s and time-to-solution at 256^3; interp GB/s vs HBM peak"
+UNIT = "matvec/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "f64", "f32"])
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution run")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def config(n, precision):
+    return {"workload": f"C3: GN Hessian matvec, synth rotation {n}^3, nt=4, cubic-Lagrange SL, FD8, "
+                        "H1 alpha=1e-2, near-incompressible beta=1e-4, SSD",
+            "grid": [n, n, n], "n_t": 4, "interp": "cubic", "precision": precision,
+            "l2": "inputs > L2 (working set several GB per matvec, no flush needed)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, val in zip(names, r[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of the gather kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(a):
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2401_17493_b200 as F
+    from paper_2401_17493_b200 import _lib as L
+
+    n = a.n
+    dtype = np.float32 if a.precision == "f32" else np.float64
+    tdt = np.float32 if a.precision in ("mixed", "f32") else None
+    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3, dtype=dtype)
+    grid = m0.grid
+    reg = F.RegConfig(alpha=1e-2, operator=F.RegOperatorSpec(1, True),
+                      incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    v = F.VectorField._wrap(grid, 0.5 * vtrue.data)
+    st = F.KktState(m0, m1, reg, distance="ssd", method="cubic", scheme="fd8", v_init=v, transport_dtype=tdt)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    vt = F.VectorField._wrap(grid, 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=grid.torch_dtype,
+                                                     device="cuda"))
+    out = torch.empty_like(vt.data)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    for _ in range(a.warmup):
+        st.hessian_matvec(vt, out=out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0 = st.matvecs
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            st.hessian_matvec(vt, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    assert st.matvecs - c0 == a.steps
+    t_ms = max_over_ranks(e0.elapsed_time(e1))
+    ms_per_step = t_ms / a.steps
+    value = world * a.steps / (t_ms / 1e3)
+
+    # launches of OUR kernels per matvec (from the host call sequence in csrc/kkt.cu:
+    # inc-state 4, adjoint 4, body force 1, combine 1) plus cuFFT transforms (9)
+    launches_per_matvec = 4 + 4 + 1 + 1
+    gpu_launches = launches_per_matvec * a.steps
+
+    # --- dominant kernel roofline: one cubic SL gather step (k_gather) -------
+    N = n ** 3
+    disp = st.trajectory.disp.to(torch.float32) if tdt is not None or dtype == np.float32 else st.trajectory.disp
+    fdt = disp.dtype
+    f = torch.randn((n, n, n), generator=gen, dtype=fdt, device="cuda")
+    g_out = torch.empty_like(f)
+    ins = (ctypes.c_void_p * 1)(f.data_ptr())
+    outs = (ctypes.c_void_p * 1)(g_out.data_ptr())
+    nn = L.n3((n, n, n))
+    fcode = L.dtype_code(fdt)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    for _ in range(3):
+        L.check(L.lib().frg_gather(nn, 3, fcode, 2, ctypes.c_void_p(disp.data_ptr()), 1, ins, outs, sp), "gather")
+    reps = 50
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(reps):
+        L.check(L.lib().frg_gather(nn, 3, fcode, 2, ctypes.c_void_p(disp.data_ptr()), 1, ins, outs, sp), "gather")
+    g1.record(stream)
+    torch.cuda.synchronize()
+    t_gather = g0.elapsed_time(g1) / reps / 1e3
+    es = 4 if fdt == torch.float32 else 8
+    alg_bytes = N * (3 * es + es + es)  # coordinates + field (once) + output
+    peak, peak_src = peaks()
+    achieved = alg_bytes / t_gather / 1e9
+    traffic = profile_traffic().get("k_gather_cubic_f32_bytes_per_launch")
+
+    # whole-matvec roofline with the canonical field-pass count (174 F)
+    canon = 174 * 4 * N
+    matvec_roofline = {"canonical_bytes": canon, "achieved_gbs": canon / (ms_per_step / 1e3) / 1e9,
+                       "peak_gbs": peak, "frac": canon / (ms_per_step / 1e3) / 1e9 / peak,
+                       "note": "SURVEY.md §8d canonical 174 fp32 field passes per matvec"}
+
+    # --- e2e through the public API with host buffers -----------------------
+    e2e_steps = max(2, min(a.steps, 5))
+    host_in = torch.empty_like(vt.data, device="cpu").pin_memory()
+    host_in.copy_(vt.data)
+    host_out = torch.empty_like(host_in).pin_memory()
+    dev_in = torch.empty_like(vt.data)
+    torch.cuda.synchronize()
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for _ in range(e2e_steps):
+        dev_in.copy_(host_in, non_blocking=True)
+        st.hessian_matvec(F.VectorField._wrap(grid, dev_in), out=out)
+        host_out.copy_(out, non_blocking=True)
+    x1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_e2e = max_over_ranks(x0.elapsed_time(x1)) / 1e3
+    e2e = {"value": world * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": host_in.numel() * host_in.element_size(),
+           "d2h_bytes_per_step": host_out.numel() * host_out.element_size(),
+           "path": "pinned host v~ -> KktState.hessian_matvec (C-ABI frg_kkt_hessian_matvec) -> pinned host"}
+
+    # --- time to solution (C3: register at 256^3, reg preconditioner) --------
+    tts = None
+    if not a.no_tts:
+        del st
+        torch.cuda.synchronize()
+        barrier()
+        F.register(m0, m1, reg=reg, precond=F.PrecondKind("reg"), method="cubic", scheme="fd8",
+                   transport_dtype=tdt, config=F.OptimizerConfig(max_outer=1))  # warm plans
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        vsol, rep = F.register(m0, m1, reg=reg, precond=F.PrecondKind("reg"), method="cubic", scheme="fd8",
+                               transport_dtype=tdt)
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        tts = {"seconds": wall, "iterations": rep.iterations, "matvecs": rep.matvecs, "pde_solves": rep.pde_solves,
+               "status": rep.status, "mismatch": rep.mismatch, "gradient": rep.gradient, "precond": "reg",
+               "detgrad_min": rep.detgrad_min}
+
+    if world > 1:
+        dist.barrier()
+    result = None
+    if rank == 0:
+        cpu = None if (a.no_cpu or world > 1) else cpu_baseline(a, m0, m1, vtrue, vt)
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 transport / f64 control" if a.precision == "mixed" else a.precision,
+            "data": "synthetic (synth_case rotation, generated on device)",
+            "config": dict(config(n, a.precision), parallelism=f"independent 256^3 problem per rank x{world}"),
+            "e2e": e2e, "gpu_launches": gpu_launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_gather<float,CUBIC> (one SL gather step)",
+                         "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather, "peak_source": peak_src},
+            "matvec_roofline": matvec_roofline,
+            "time_to_solution": tts,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(result))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def cpu_baseline(a, m0, m1, vtrue, vt):
+    """Oracle port on the host cores: one full 256^3 matvec (refresh untimed)."""
+    import numpy as np
+
+    from oracle import flowreg_oracle as O
+
+    cores = os.cpu_count() or 1
+    M0 = m0.values.double().cpu().numpy()
+    M1 = m1.values.double().cpu().numpy()
+    V = 0.5 * vtrue.data.double().cpu().numpy()
+    VT = vt.data.double().cpu().numpy()
+    st = O.Kkt(M0, M1, O.Reg(alpha=1e-2, incomp="near-incompressible", beta=1e-4), 4, "ssd", "cubic", "fd8", V)
+    t0 = time.perf_counter()
+    st.hessian_matvec(VT)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"1 Hessian matvec at {a.n}^3 f64 (oracle/flowreg_oracle.py, C/OpenMP gathers + "
+                      f"scipy pocketfft, {cores} threads); refresh excluded"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU oracle port)
+# ---------------------------------------------------------------------------
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import numpy as np
+
+    from oracle import flowreg_oracle as O
+
+    n = a.n
+    cores = os.cpu_count() or 1
+    # inputs: the oracle's own synth (64-step cubic transport); bounded run
+    m0, m1, vtrue = O.synth_case("rotation", n, seed=1, d=3, ref_steps=64)
+    st = O.Kkt(m0, m1, O.Reg(alpha=1e-2, incomp="near-incompressible", beta=1e-4), 4, "ssd", "cubic", "fd8",
+               0.5 * vtrue)
+    vt = 0.1 * np.random.default_rng(0).standard_normal(vtrue.shape)
+    warm = min(a.warmup, 1)
+    steps = max(1, min(a.steps, 2))
+    for _ in range(warm):
+        st.hessian_matvec(vt)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.hessian_matvec(vt)
+    dt = time.perf_counter() - t0
+    value = steps / dt
+    sample = (f"{steps} timed + {warm} warm-up Hessian matvecs at {n}^3 (f64 oracle port, {cores} host threads); "
+              f"bounded from --steps {a.steps} --warmup {a.warmup} to keep the run within minutes")
+    res = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": steps,
+           "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle synth_case rotation)",
+           "config": config(n, "f64"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res))
+    return res
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -220,7 +220,8 @@ void convert(int sdtype, const void* src, int ddtype, void* dst, long long n, cu
 template <typename T>
 __global__ void k_axpby(T a, const T* __restrict__ x, T b, T* __restrict__ y, long long n) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) y[i] = a * x[i] + b * y[i];
+    // b == 0 must not read y (it may be uninitialised, 0 * NaN = NaN)
+    if (i < n) y[i] = (b == T(0)) ? a * x[i] : a * x[i] + b * y[i];
 }
 
 void axpby(int dtype, double a, const void* x, double b, void* y, long long n, cudaStream_t st) {
