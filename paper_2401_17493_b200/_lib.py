@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflowreg_b200.so")
+LIB_PATH = os.environ.get("FRG_LIB", os.path.join(HERE, "libflowreg_b200.so"))
 
 F32, F64, I32 = 0, 1, 2
 METHODS = {"nearest": 0, "linear": 1, "cubic": 2}

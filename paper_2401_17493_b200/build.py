@@ -37,10 +37,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu and link libflowreg_b200.so (``out`` + ``extra``
+    flags build an experimental variant elsewhere)."""
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
-    objdir = os.path.join(HERE, "_build")
+    objdir = os.path.join(os.path.dirname(lib), "_build") if out else os.path.join(HERE, "_build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -53,27 +56,29 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = False
     for cmd, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0:
             failed = True
-            sys.stderr.write(" ".join(cmd) + "\n" + out + "\n")
-        elif verbose and out:
-            sys.stderr.write(out)
+            sys.stderr.write(" ".join(cmd) + "\n" + log + "\n")
+        elif verbose and log:
+            sys.stderr.write(log)
     if failed:
         raise RuntimeError("nvcc failed building libflowreg_b200")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="variant output path")
+    ap.add_argument("-D", action="append", default=[], help="extra -D defines for a variant")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, extra=[f"-D{d}" for d in a.D], out=a.out))
 
 
 if __name__ == "__main__":

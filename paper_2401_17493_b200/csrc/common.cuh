@@ -97,34 +97,51 @@ struct Real<double> {
 };
 
 // Lagrange cubic weights for nodes at offsets -1, 0, 1, 2 (_kernels.py:162-167)
+// (divisions by 6 and 2 replaced by multiplications: no FCHK/slow-path division
+// per weight; the difference is within one rounding of the reference's weights)
 template <typename T>
 __device__ __forceinline__ void lagrange4(T t, T w[4]) {
-    const T one = T(1), two = T(2);
-    w[0] = -t * (t - one) * (t - two) / T(6);
-    w[1] = (t + one) * (t - one) * (t - two) / two;
-    w[2] = -(t + one) * t * (t - two) / two;
-    w[3] = (t + one) * t * (t - one) / T(6);
+    const T one = T(1), two = T(2), sixth = T(1.0 / 6.0), half = T(0.5);
+    const T tm1 = t - one, tm2 = t - two, tp1 = t + one;
+    w[0] = -t * tm1 * tm2 * sixth;
+    w[1] = tp1 * tm1 * tm2 * half;
+    w[2] = -tp1 * t * tm2 * half;
+    w[3] = tp1 * t * tm1 * sixth;
+}
+
+// Periodic wrap of an index that is usually inside [0, n) or within a few
+// periods of it: one unsigned compare on the common path, % only on wrap.
+__device__ __forceinline__ int wrap_near(int b, int n) {
+    if ((unsigned)b >= (unsigned)n) {
+        b %= n;
+        if (b < 0) b += n;
+    }
+    return b;
 }
 
 // Per-axis stencil: wrapped node indices (already multiplied by the axis
-// stride) and weights.  NT = taps per axis (1 nearest, 2 linear, 4 cubic).
+// stride, 32-bit: N < 2^31 for every grid up to 1024^3) and weights.
+// NT = taps per axis (1 nearest, 2 linear, 4 cubic).
 template <typename T, int NT>
 struct Axis {
     int off[NT];
     T w[NT];
 };
 
-// Build the axis stencil for fractional position base + frac where `base` is
-// an integer node index (may be outside [0, n)) and frac in [0, 1).
+template <int M>
+struct Taps {
+    static constexpr int value = (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1));
+};
+
+// Build the axis stencil for node `base` (any integer, wrapped here) and
+// fractional offset t in [0, 1).  For NEAREST, base = floor(q + 0.5).
 template <typename T, int M>
-__device__ __forceinline__ void axis_stencil(long long fl, T t, int n, int stride,
-                                             Axis<T, (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1))>& ax) {
+__device__ __forceinline__ void axis_stencil(int base, T t, int n, int stride, Axis<T, Taps<M>::value>& ax) {
     if (M == NEAREST) {
-        // caller passes fl = floor(q + 0.5), t unused
-        ax.off[0] = pmod(fl, n) * stride;
+        ax.off[0] = wrap_near(base, n) * stride;
         ax.w[0] = T(1);
     } else if (M == LINEAR) {
-        int i0 = pmod(fl, n);
+        int i0 = wrap_near(base, n);
         int i1 = i0 + 1;
         if (i1 >= n) i1 -= n;
         ax.off[0] = i0 * stride;
@@ -141,12 +158,11 @@ __device__ __forceinline__ void axis_stencil(long long fl, T t, int n, int strid
                 ax.w[a] = w[a];
             }
         } else {
-            int b = pmod(fl - 1, n);
+            int b = wrap_near(base - 1, n);
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 int x = b + a;
-                if (x >= n) x -= n;
-                if (x >= n) x -= n;  // n >= 2 covers every n the grids allow
+                if (x >= n) x -= n;  // n >= 4 for every axis longer than 1
                 ax.off[a] = x * stride;
                 ax.w[a] = w[a];
             }
@@ -154,47 +170,46 @@ __device__ __forceinline__ void axis_stencil(long long fl, T t, int n, int strid
     }
 }
 
-template <int M>
-struct Taps {
-    static constexpr int value = (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1));
-};
-
 // Full tensor-product stencil for one query point.
 template <typename T, int M>
 struct Stencil {
     Axis<T, Taps<M>::value> a0, a1, a2;
 };
 
-// Query point given as fractional indices (q0, q1, q2) in the storage type
-// accuracy of `T` (double for the generic sample_nd boundary).
-template <typename T, int M>
-__device__ __forceinline__ void make_stencil_q(const Dims& g, T q0, T q1, T q2, Stencil<T, M>& s) {
+// floor(q) of an arbitrary f64 fractional index reduced into [0, n) first,
+// so huge coordinates keep Python floor-mod semantics (_kernels.py:107-118).
+__device__ __forceinline__ int reduce_index(double fl, int n) { return pmod((long long)fl, n); }
+
+// Query point given as f64 fractional indices (the sample_nd boundary).
+template <int M>
+__device__ __forceinline__ void make_stencil_q(const Dims& g, double q0, double q1, double q2,
+                                               Stencil<double, M>& s) {
     if (M == NEAREST) {
-        axis_stencil<T, M>((long long)Real<T>::floor_(q0 + T(0.5)), T(0), g.n0, g.n1 * g.n2, s.a0);
-        axis_stencil<T, M>((long long)Real<T>::floor_(q1 + T(0.5)), T(0), g.n1, g.n2, s.a1);
-        axis_stencil<T, M>((long long)Real<T>::floor_(q2 + T(0.5)), T(0), g.n2, 1, s.a2);
+        axis_stencil<double, M>(reduce_index(floor(q0 + 0.5), g.n0), 0.0, g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<double, M>(reduce_index(floor(q1 + 0.5), g.n1), 0.0, g.n1, g.n2, s.a1);
+        axis_stencil<double, M>(reduce_index(floor(q2 + 0.5), g.n2), 0.0, g.n2, 1, s.a2);
     } else {
-        T f0 = Real<T>::floor_(q0), f1 = Real<T>::floor_(q1), f2 = Real<T>::floor_(q2);
-        axis_stencil<T, M>((long long)f0, q0 - f0, g.n0, g.n1 * g.n2, s.a0);
-        axis_stencil<T, M>((long long)f1, q1 - f1, g.n1, g.n2, s.a1);
-        axis_stencil<T, M>((long long)f2, q2 - f2, g.n2, 1, s.a2);
+        double f0 = floor(q0), f1 = floor(q1), f2 = floor(q2);
+        axis_stencil<double, M>(reduce_index(f0, g.n0), q0 - f0, g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<double, M>(reduce_index(f1, g.n1), q1 - f1, g.n1, g.n2, s.a1);
+        axis_stencil<double, M>(reduce_index(f2, g.n2), q2 - f2, g.n2, 1, s.a2);
     }
 }
 
-// Query point = grid node (i, j, k) + displacement (in index units).  The
+// Query point = grid node (i, j, k) + displacement (index units).  The
 // integer part is split off exactly, so precision does not degrade with n.
 template <typename T, int M>
 __device__ __forceinline__ void make_stencil_disp(const Dims& g, int i, int j, int k, T d0, T d1, T d2,
                                                   Stencil<T, M>& s) {
     if (M == NEAREST) {
-        axis_stencil<T, M>(i + (long long)Real<T>::floor_(d0 + T(0.5)), T(0), g.n0, g.n1 * g.n2, s.a0);
-        axis_stencil<T, M>(j + (long long)Real<T>::floor_(d1 + T(0.5)), T(0), g.n1, g.n2, s.a1);
-        axis_stencil<T, M>(k + (long long)Real<T>::floor_(d2 + T(0.5)), T(0), g.n2, 1, s.a2);
+        axis_stencil<T, M>(i + (int)Real<T>::floor_(d0 + T(0.5)), T(0), g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>(j + (int)Real<T>::floor_(d1 + T(0.5)), T(0), g.n1, g.n2, s.a1);
+        axis_stencil<T, M>(k + (int)Real<T>::floor_(d2 + T(0.5)), T(0), g.n2, 1, s.a2);
     } else {
         T f0 = Real<T>::floor_(d0), f1 = Real<T>::floor_(d1), f2 = Real<T>::floor_(d2);
-        axis_stencil<T, M>(i + (long long)f0, d0 - f0, g.n0, g.n1 * g.n2, s.a0);
-        axis_stencil<T, M>(j + (long long)f1, d1 - f1, g.n1, g.n2, s.a1);
-        axis_stencil<T, M>(k + (long long)f2, d2 - f2, g.n2, 1, s.a2);
+        axis_stencil<T, M>(i + (int)f0, d0 - f0, g.n0, g.n1 * g.n2, s.a0);
+        axis_stencil<T, M>(j + (int)f1, d1 - f1, g.n1, g.n2, s.a1);
+        axis_stencil<T, M>(k + (int)f2, d2 - f2, g.n2, 1, s.a2);
     }
 }
 
@@ -204,14 +219,14 @@ template <typename A, typename T, int M, typename V>
 __device__ __forceinline__ A apply_stencil(const V* __restrict__ f, const Stencil<T, M>& s) {
     constexpr int NT = Taps<M>::value;
     if (M == NEAREST) {
-        return (A)__ldg(f + (long long)s.a0.off[0] + s.a1.off[0] + s.a2.off[0]);
+        return (A)__ldg(f + (s.a0.off[0] + s.a1.off[0] + s.a2.off[0]));
     } else if (M == LINEAR) {
         A c[2][2];
 #pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
-                const V* row = f + (long long)s.a0.off[a] + s.a1.off[b];
+                const V* row = f + (s.a0.off[a] + s.a1.off[b]);
                 c[a][b] = (A(1) - (A)s.a2.w[1]) * (A)__ldg(row + s.a2.off[0]) +
                           (A)s.a2.w[1] * (A)__ldg(row + s.a2.off[1]);
             }
@@ -225,7 +240,7 @@ __device__ __forceinline__ A apply_stencil(const V* __restrict__ f, const Stenci
             A plane = A(0);
 #pragma unroll
             for (int b = 0; b < NT; ++b) {
-                const V* row = f + (long long)s.a0.off[a] + s.a1.off[b];
+                const V* row = f + (s.a0.off[a] + s.a1.off[b]);
                 A r = A(0);
 #pragma unroll
                 for (int c = 0; c < NT; ++c) r += (A)s.a2.w[c] * (A)__ldg(row + s.a2.off[c]);
@@ -235,6 +250,28 @@ __device__ __forceinline__ A apply_stencil(const V* __restrict__ f, const Stenci
         }
         return acc;
     }
+}
+
+// ---------------------------------------------------------------------------
+// voxel launch geometry: block (32, 8) over (k, j), grid z over i.  No
+// integer division anywhere; the flat index fits in 32 bits.
+// ---------------------------------------------------------------------------
+constexpr int BX = 32, BY = 8;
+
+struct Vox {
+    int i, j, k, p;
+};
+
+inline dim3 vox_grid(const Dims& g) { return dim3((g.n2 + BX - 1) / BX, (g.n1 + BY - 1) / BY, g.n0); }
+inline dim3 vox_block() { return dim3(BX, BY, 1); }
+
+__device__ __forceinline__ bool vox(const Dims& g, Vox& v) {
+    v.k = blockIdx.x * BX + threadIdx.x;
+    v.j = blockIdx.y * BY + threadIdx.y;
+    v.i = blockIdx.z;
+    if (v.k >= g.n2 || v.j >= g.n1) return false;
+    v.p = (v.i * g.n1 + v.j) * g.n2 + v.k;
+    return true;
 }
 
 // flat index -> (i, j, k)

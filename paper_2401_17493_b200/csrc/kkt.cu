@@ -44,7 +44,7 @@ struct KktCtx {
     int n_t, method, scheme, distance, tdt, cdt;
     RegSpec reg;
     cudaStream_t st;
-    PlanCache plans;
+    PlanCache& plans = shared_plans();
     Workspace ws_a, ws_b, ws_c;
     DevBuf m0, m1, v, vT, negv, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
     DevBuf vtT, vty, mt, lt, bf, disp_trial, mtrial, gmC, tmp1, tmp2, tmp3;
@@ -127,7 +127,6 @@ void kkt_destroy(KktCtx* k) {
     k->ws_a.release();
     k->ws_b.release();
     k->ws_c.release();
-    k->plans.clear();
     delete k;
 }
 
@@ -295,18 +294,30 @@ double kkt_objective_at(KktCtx* k, const void* v_trial) {
     return dist_value(k, mfin) + reg_energy_c(k, v_trial);
 }
 
-// out = alpha L a + P[b_T]  (kkt.py:233-235, 259-260)
-static void reg_plus_body(KktCtx* k, const void* a, const void* bT, void* out) {
+// out = alpha L a + P[b]  (kkt.py:233-235, 259-260)
+//  incomp none : alpha L a by one D2Z / scale / Z2D round trip straight into
+//                `out`, then the trapezoid body force is accumulated into it by
+//                the body-force kernel (no transform of b at all);
+//  otherwise   : D2Z(a) + R2C(b) (b in transport precision: the projection
+//                multiplier is bounded by 1, nothing amplifies its rounding),
+//                one fused combine kernel, one Z2D.
+static void reg_plus_body(KktCtx* k, const void* a, const void* lam_series, void* out) {
+    if (k->reg.incomp == 0) {
+        size_t need = spectral_ws_bytes(k->g, k->cdt, k->g.d);
+        spectral_apply_ex(k->plans, k->ws_a.get(need), k->g, k->cdt, k->g.d, a, out, SK_REG, k->reg, k->st);
+        body_force(k->g, k->tdt, k->cdt, k->n_t, lam_series, k->grads.p, out, true, k->st);
+        return;
+    }
+    body_force(k->g, k->tdt, k->tdt, k->n_t, lam_series, k->grads.p, k->bf.p, false, k->st);
     size_t sa = (size_t)half_len(k->g) * (k->C() == 8 ? 16 : 8) * k->g.d + (size_t)half_len(k->g) * 8;
     size_t sb = (size_t)half_len(k->g) * (k->T() == 8 ? 16 : 8) * k->g.d;
-    reg_plus_project_ex(k->plans, k->ws_a.get(sa), k->ws_b.get(sb), k->g, k->cdt, a, k->tdt, bT, out, k->reg,
-                        k->reg.incomp != 0, k->st);
+    reg_plus_project_ex(k->plans, k->ws_a.get(sa), k->ws_b.get(sb), k->g, k->cdt, a, k->tdt, k->bf.p, out, k->reg,
+                        true, k->st);
 }
 
 void kkt_gradient(KktCtx* k, void* g_out) {
     FRG_REQUIRE(k->have_state, "refresh first");
-    body_force(k->g, k->tdt, k->tdt, k->n_t, k->lam.p, k->grads.p, k->bf.p, false, k->st);
-    reg_plus_body(k, k->v.p, k->bf.p, g_out);
+    reg_plus_body(k, k->v.p, k->lam.p, g_out);
 }
 
 void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
@@ -326,8 +337,7 @@ void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
     solve_adjoint(k->g, k->tdt, k->method, k->n_t, k->disp_b.p, k->cmul.p, k->lt.p, k->st);
     k->matvecs += 1;
     k->pde_solves += 2;
-    body_force(k->g, k->tdt, k->tdt, k->n_t, k->lt.p, k->grads.p, k->bf.p, false, k->st);
-    reg_plus_body(k, vt, k->bf.p, out);
+    reg_plus_body(k, vt, k->lt.p, out);
 }
 
 double kkt_mismatch(KktCtx* k) {

@@ -75,6 +75,8 @@ void xpay_to(int dtype, const void* x, double a, const void* y, void* z, long lo
 double pcg_update(int dtype, double k, const void* s, const void* hs, void* x, void* r, long long n,
                   cudaStream_t st);
 void fill(int dtype, void* a, double value, long long n, cudaStream_t st);
+// out (odtype) += src (sdtype)
+void add_into(int odtype, void* out, int sdtype, const void* src, long long n, cudaStream_t st);
 void scale_diff(int dtype, const void* a, const void* b, double sa, void* out, long long n,
                 cudaStream_t st);  // out = sa*(a - b)
 // out = c1*a + c2*b + c3*c  (pointwise, same dtype; b/c may be null)

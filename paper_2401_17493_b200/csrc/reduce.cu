@@ -288,6 +288,25 @@ double pcg_update(int dtype, double k, const void* s, const void* hs, void* x, v
     return g_scratch.host[0];
 }
 
+template <typename O, typename S>
+__global__ void k_add_into(O* __restrict__ out, const S* __restrict__ src, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = out[i] + (O)src[i];
+}
+
+void add_into(int odtype, void* out, int sdtype, const void* src, long long n, cudaStream_t st) {
+    int nb = blocks_for(n, P_TPB);
+    if (odtype == F64 && sdtype == F64)
+        k_add_into<double, double><<<nb, P_TPB, 0, st>>>((double*)out, (const double*)src, n);
+    else if (odtype == F64 && sdtype == F32)
+        k_add_into<double, float><<<nb, P_TPB, 0, st>>>((double*)out, (const float*)src, n);
+    else if (odtype == F32 && sdtype == F32)
+        k_add_into<float, float><<<nb, P_TPB, 0, st>>>((float*)out, (const float*)src, n);
+    else
+        throw Error(E_ARG, "add_into: unsupported dtypes");
+    FRG_CHECK_LAUNCH();
+}
+
 template <typename T>
 __global__ void k_fill(T* a, T v, long long n) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

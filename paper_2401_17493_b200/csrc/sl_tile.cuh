@@ -1,0 +1,405 @@
+// Shared-memory tiled semi-Lagrangian gather engine (sm_100a).
+//
+// One CTA owns an output tile of BX x BY x TI voxels (k fastest).  Each
+// thread reads the displacement of its TI voxels, the CTA reduces the
+// bounding box of every interpolation stencil in the tile (for the synthetic
+// velocities a tile's departure points move coherently, so the box is the
+// tile plus the intra-tile displacement spread plus 3 halo planes), stages
+// each gathered field's box into shared memory with coalesced row loads
+// (periodic wrap applied on load, optional f64->f32 conversion), and then
+// evaluates the 64-tap cubic (8-tap linear, 1-tap nearest) stencils from
+// shared memory.  Tiles whose box exceeds the shared-memory budget fall back
+// to direct (L1/L2) gathers, so any displacement field is handled.
+//
+// The Op functor supplies: the displacement of a voxel (disp), the NF field
+// pointers (field), and the pointwise epilogue (done) that consumes the NF
+// gathered values — so every SL time step of the state, adjoint,
+// incremental state / adjoint, RK2 departure, deformation-tensor and
+// composition solves is ONE kernel.
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace frg {
+
+#ifndef SL_TI_OVERRIDE
+#define SL_TI_OVERRIDE 4
+#endif
+constexpr int SL_TI = SL_TI_OVERRIDE;  // voxels per thread along axis 0
+#ifndef FRG_SL_PAIRED
+#define FRG_SL_PAIRED 0
+#endif
+
+// box budget per CTA: 24 KB for fp32 (several CTAs per SM), 44 KB for the
+// f64 parity path (static shared memory is limited to 48 KB)
+template <typename T>
+struct BoxCap {
+    static constexpr int value = (sizeof(T) == 4 ? 32 * 1024 : 44 * 1024) / (int)sizeof(T);
+};
+
+// asynchronous global -> shared copy of one element (LDGSTS), no register staging
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Stage box rows [lo0.., lo1.., lo2..] of field src into smem.  One warp per
+// box row, lanes along the contiguous axis; every copy is issued before any
+// is waited on, so the whole box is in flight at once.
+// floor(e / d) for e, d < 2^16 with one IMAD.HI: m = floor(2^32 / d) + 1
+__device__ __forceinline__ unsigned fast_div(unsigned e, unsigned m) { return __umulhi(e, m); }
+__host__ __device__ __forceinline__ unsigned div_magic(unsigned d) {
+    // floor((2^32 - 1) / d) + 1: exact floor(e / d) for e, d < 2^16 (32-bit division only)
+    return 0xFFFFFFFFu / d + 1u;
+}
+
+// Two cubic stencils evaluated together with the Blackwell paired fp32 FMA
+// (FFMA2: __ffma2_rn / __fmul2_rn), halving the FP instruction count; the taps
+// are still scalar shared-memory loads.  Lane .x = point A, .y = point B.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ void lagrange4_x2(float2 t, float2 w[4]) {
+    const float2 one = f2(1.f, 1.f), two = f2(2.f, 2.f);
+    const float2 tm1 = __fadd2_rn(t, f2(-1.f, -1.f)), tm2 = __fadd2_rn(t, f2(-2.f, -2.f)),
+                 tp1 = __fadd2_rn(t, one);
+    const float2 sixth = f2(1.f / 6.f, 1.f / 6.f), half = f2(0.5f, 0.5f);
+    const float2 mt = f2(-t.x, -t.y), mtp1 = f2(-tp1.x, -tp1.y);
+    w[0] = __fmul2_rn(__fmul2_rn(__fmul2_rn(mt, tm1), tm2), sixth);
+    w[1] = __fmul2_rn(__fmul2_rn(__fmul2_rn(tp1, tm1), tm2), half);
+    w[2] = __fmul2_rn(__fmul2_rn(__fmul2_rn(mtp1, t), tm2), half);
+    w[3] = __fmul2_rn(__fmul2_rn(__fmul2_rn(tp1, t), tm1), sixth);
+    (void)two;
+}
+
+__device__ __forceinline__ float2 box_cubic_x2(const float* __restrict__ box, int S1, int S2, int oA, int oB,
+                                               float2 t0, float2 t1, float2 t2) {
+    float2 w0[4], w1[4], w2[4];
+    lagrange4_x2(t0, w0);
+    lagrange4_x2(t1, w1);
+    lagrange4_x2(t2, w2);
+    const int sa = S1 * S2;
+    const float* pA = box + oA;
+    const float* pB = box + oB;
+    float2 acc = f2(0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const float* rA = pA;
+        const float* rB = pB;
+        float2 plane = f2(0.f, 0.f);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+            float2 r = __fmul2_rn(w2[0], f2(rA[0], rB[0]));
+            r = __ffma2_rn(w2[1], f2(rA[1], rB[1]), r);
+            r = __ffma2_rn(w2[2], f2(rA[2], rB[2]), r);
+            r = __ffma2_rn(w2[3], f2(rA[3], rB[3]), r);
+            plane = __ffma2_rn(w1[bb], r, plane);
+            rA += S2;
+            rB += S2;
+        }
+        acc = __ffma2_rn(w0[a], plane, acc);
+        pA += sa;
+        pB += sa;
+    }
+    return acc;
+}
+
+// The box is flattened over all CTA threads (e = tid + 256 r), row / column
+// recovered with multiply-high magic division — no integer division, every
+// lane busy whatever the row length.
+template <typename T, typename V>
+__device__ __forceinline__ void stage_box(T* __restrict__ box, const V* __restrict__ src, const Dims& g, int lo0,
+                                          int lo1, int lo2, int S1, int S2, int S2p, int vol, int tid) {
+    const unsigned m2 = div_magic((unsigned)S2), m1 = div_magic((unsigned)S1);
+    const bool inner_k = lo2 >= 0 && lo2 + S2 <= g.n2;
+    auto addr = [&](int e, const V*& s, T*& d) {
+        const int r = (int)fast_div((unsigned)e, m2);
+        const int c = e - r * S2;
+        const int a = (int)fast_div((unsigned)r, m1);
+        const int b = r - a * S1;
+        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1);
+        const int gk = inner_k ? lo2 + c : wrap_near(lo2 + c, g.n2);
+        s = src + ((gi * g.n1 + gj) * g.n2 + gk);
+        d = box + (r * S2p + c);
+    };
+    if constexpr (sizeof(T) == sizeof(V)) {
+        for (int e = tid; e < vol; e += BX * BY) {
+            const V* s;
+            T* d;
+            addr(e, s, d);
+            cp_async_elem<sizeof(T)>(d, s);
+        }
+        cp_async_wait_all();
+    } else {
+        // converting copy through registers: batches of 8 independent loads in flight
+        constexpr int B = 8;
+        for (int e0 = tid; e0 < vol; e0 += B * BX * BY) {
+            V v[B];
+            T* d[B];
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int e = e0 + q * BX * BY;
+                const V* s;
+                d[q] = nullptr;
+                if (e < vol) {
+                    addr(e, s, d[q]);
+                    v[q] = __ldg(s);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (d[q]) *d[q] = (T)v[q];
+        }
+    }
+}
+
+template <int M>
+struct Halo {
+    static constexpr int lo = (M == CUBIC ? 1 : 0);
+    static constexpr int hi = (M == CUBIC ? 2 : (M == LINEAR ? 1 : 0));
+};
+
+__device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ int warp_max_i(int v) { return __reduce_max_sync(0xffffffffu, v); }
+
+// evaluate one stencil from the staged box (no wrap needed inside the box)
+template <typename T, int M>
+__device__ __forceinline__ T box_interp(const T* __restrict__ box, int S1, int S2, int r0, int r1, int r2, T t0,
+                                        T t1, T t2) {
+    // r_a = (base_a - lo_a): box coordinate of the first tap
+    if (M == NEAREST) {
+        return box[(r0 * S1 + r1) * S2 + r2];
+    } else if (M == LINEAR) {
+        const T* b = box + (r0 * S1 + r1) * S2 + r2;
+        T c00 = (T(1) - t2) * b[0] + t2 * b[1];
+        T c01 = (T(1) - t2) * b[S2] + t2 * b[S2 + 1];
+        T c10 = (T(1) - t2) * b[S1 * S2] + t2 * b[S1 * S2 + 1];
+        T c11 = (T(1) - t2) * b[S1 * S2 + S2] + t2 * b[S1 * S2 + S2 + 1];
+        return (T(1) - t0) * ((T(1) - t1) * c00 + t1 * c01) + t0 * ((T(1) - t1) * c10 + t1 * c11);
+    } else {
+        T w0[4], w1[4], w2[4];
+        lagrange4(t0, w0);
+        lagrange4(t1, w1);
+        lagrange4(t2, w2);
+        const int sa = S1 * S2;
+        const T* p0 = box + ((r0 * S1 + r1) * S2 + r2);
+        T acc = T(0);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const T* row = p0;
+            T plane = T(0);
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+                T r = w2[0] * row[0];
+                r += w2[1] * row[1];
+                r += w2[2] * row[2];
+                r += w2[3] * row[3];
+                plane += w1[bb] * r;
+                row += S2;
+            }
+            acc += w0[a] * plane;
+            p0 += sa;
+        }
+        return acc;
+    }
+}
+
+// stencil from a (wrapped) node base and fractional part, evaluated in global memory
+template <typename T, int M, typename V>
+__device__ __forceinline__ T global_interp(const Dims& g, const V* __restrict__ f, int b0, int b1, int b2, T t0, T t1,
+                                           T t2) {
+    Stencil<T, M> s;
+    axis_stencil<T, M>(b0, t0, g.n0, g.n1 * g.n2, s.a0);
+    axis_stencil<T, M>(b1, t1, g.n1, g.n2, s.a1);
+    axis_stencil<T, M>(b2, t2, g.n2, 1, s.a2);
+    return apply_stencil<T, T, M, V>(f, s);
+}
+
+// Generic tiled SL kernel.  T: arithmetic / box type; Op::V: source type of
+// the gathered fields (may be wider than T: converted on staging).
+template <typename T, int M, int NF, class Op>
+__global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) k_sl(Dims g, Op op) {
+    __shared__ __align__(16) T box[BoxCap<T>::value];
+    __shared__ int red[6][BY];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int k = blockIdx.x * BX + tx;
+    const int j = blockIdx.y * BY + ty;
+    const int i_base = blockIdx.z * SL_TI;
+    const bool in_kj = (k < g.n2) && (j < g.n1);
+
+    int base0[SL_TI], base1[SL_TI], base2[SL_TI];
+    T fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
+    int mn0 = INT_MAX, mn1 = INT_MAX, mn2 = INT_MAX, mx0 = INT_MIN, mx1 = INT_MIN, mx2 = INT_MIN;
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const int i = i_base + u;
+        base0[u] = base1[u] = base2[u] = 0;
+        fr0[u] = fr1[u] = fr2[u] = T(0);
+        if (in_kj && i < g.n0) {
+            const int p = (i * g.n1 + j) * g.n2 + k;
+            T d0, d1, d2;
+            op.disp(p, d0, d1, d2);
+            if (M == NEAREST) {
+                d0 += T(0.5);
+                d1 += T(0.5);
+                d2 += T(0.5);
+            }
+            T f0 = Real<T>::floor_(d0), f1 = Real<T>::floor_(d1), f2 = Real<T>::floor_(d2);
+            base0[u] = i + (int)f0;
+            base1[u] = j + (int)f1;
+            base2[u] = k + (int)f2;
+            fr0[u] = d0 - f0;
+            fr1[u] = d1 - f1;
+            fr2[u] = d2 - f2;
+            mn0 = min(mn0, base0[u]);
+            mx0 = max(mx0, base0[u]);
+            mn1 = min(mn1, base1[u]);
+            mx1 = max(mx1, base1[u]);
+            mn2 = min(mn2, base2[u]);
+            mx2 = max(mx2, base2[u]);
+        }
+    }
+    // CTA-wide bounding box of the stencil bases
+    mn0 = warp_min_i(mn0);
+    mn1 = warp_min_i(mn1);
+    mn2 = warp_min_i(mn2);
+    mx0 = warp_max_i(mx0);
+    mx1 = warp_max_i(mx1);
+    mx2 = warp_max_i(mx2);
+    if (tx == 0) {
+        red[0][ty] = mn0;
+        red[1][ty] = mn1;
+        red[2][ty] = mn2;
+        red[3][ty] = mx0;
+        red[4][ty] = mx1;
+        red[5][ty] = mx2;
+    }
+    __syncthreads();
+    mn0 = red[0][0];
+    mn1 = red[1][0];
+    mn2 = red[2][0];
+    mx0 = red[3][0];
+    mx1 = red[4][0];
+    mx2 = red[5][0];
+#pragma unroll
+    for (int w = 1; w < BY; ++w) {
+        mn0 = min(mn0, red[0][w]);
+        mn1 = min(mn1, red[1][w]);
+        mn2 = min(mn2, red[2][w]);
+        mx0 = max(mx0, red[3][w]);
+        mx1 = max(mx1, red[4][w]);
+        mx2 = max(mx2, red[5][w]);
+    }
+    if (mn0 == INT_MAX) return;  // empty tile (uniform across the CTA)
+    const int lo0 = mn0 - Halo<M>::lo, lo1 = mn1 - Halo<M>::lo, lo2 = mn2 - Halo<M>::lo;
+    const int S0 = mx0 + Halo<M>::hi - lo0 + 1;
+    const int S1 = mx1 + Halo<M>::hi - lo1 + 1;
+    const int S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    // rows padded to 32 elements: lanes of a warp on different box rows then
+    // never hit the same shared-memory bank (their columns differ by < 32)
+    const int S2p = (S2 + 31) & ~31;
+    const long long vol = (long long)S0 * S1 * S2;
+    const bool fits = (long long)S0 * S1 * S2p <= BoxCap<T>::value;
+
+    T vals[SL_TI][NF];
+    if (fits) {
+        const int tid = ty * BX + tx;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            if (f > 0) __syncthreads();
+            stage_box<T, typename Op::V>(box, op.field(f), g, lo0, lo1, lo2, S1, S2, S2p, (int)vol, tid);
+            __syncthreads();
+            if constexpr (FRG_SL_PAIRED && M == CUBIC && sizeof(T) == 4 && SL_TI % 2 == 0) {
+                // paired FFMA2 evaluation; an inactive partner reuses its twin's taps
+#pragma unroll
+                for (int u = 0; u < SL_TI; u += 2) {
+                    const bool va = in_kj && i_base + u < g.n0, vb = in_kj && i_base + u + 1 < g.n0;
+                    if (!va) {
+                        vals[u][f] = vals[u + 1][f] = T(0);
+                        continue;
+                    }
+                    const int ub = vb ? u + 1 : u;
+                    const int oA = ((base0[u] - 1 - lo0) * S1 + (base1[u] - 1 - lo1)) * S2p + (base2[u] - 1 - lo2);
+                    const int oB =
+                        ((base0[ub] - 1 - lo0) * S1 + (base1[ub] - 1 - lo1)) * S2p + (base2[ub] - 1 - lo2);
+                    float2 r = box_cubic_x2((const float*)box, S1, S2p, oA, oB, f2(fr0[u], fr0[ub]),
+                                            f2(fr1[u], fr1[ub]), f2(fr2[u], fr2[ub]));
+                    vals[u][f] = r.x;
+                    vals[u + 1][f] = vb ? r.y : T(0);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < SL_TI; ++u)
+                    vals[u][f] = (in_kj && i_base + u < g.n0)
+                                     ? box_interp<T, M>(box, S1, S2p, base0[u] - Halo<M>::lo - lo0,
+                                                        base1[u] - Halo<M>::lo - lo1, base2[u] - Halo<M>::lo - lo2,
+                                                        fr0[u], fr1[u], fr2[u])
+                                     : T(0);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const typename Op::V* src = op.field(f);
+#pragma unroll
+            for (int u = 0; u < SL_TI; ++u)
+                vals[u][f] = (in_kj && i_base + u < g.n0)
+                                 ? global_interp<T, M, typename Op::V>(g, src, base0[u], base1[u], base2[u], fr0[u],
+                                                                       fr1[u], fr2[u])
+                                 : T(0);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const int i = i_base + u;
+        if (in_kj && i < g.n0) op.done((i * g.n1 + j) * g.n2 + k, vals[u]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// displacement sources (per grid axis; axis 0 is absent in 2D)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DispSrc {
+    const T* a[3];
+    __device__ __forceinline__ void get(int p, T& d0, T& d1, T& d2) const {
+        d0 = a[0] ? a[0][p] : T(0);
+        d1 = a[1][p];
+        d2 = a[2][p];
+    }
+};
+
+template <typename T>
+inline DispSrc<T> disp_src(const Dims& g, const T* disp) {
+    DispSrc<T> s;
+    s.a[0] = s.a[1] = s.a[2] = nullptr;
+    for (int c = 0; c < g.d; ++c) s.a[g.comp_axis(c)] = disp + (size_t)c * g.N;
+    return s;
+}
+
+inline int tcode(float) { return F32; }
+inline int tcode(double) { return F64; }
+
+
+inline dim3 sl_grid(const Dims& g) {
+    return dim3((g.n2 + BX - 1) / BX, (g.n1 + BY - 1) / BY, (g.n0 + SL_TI - 1) / SL_TI);
+}
+
+template <typename T, int NF, class Op>
+void launch_sl(const Dims& g, int method, const Op& op, cudaStream_t st) {
+    switch (method) {
+        case NEAREST: k_sl<T, NEAREST, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
+        case LINEAR: k_sl<T, LINEAR, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
+        case CUBIC: k_sl<T, CUBIC, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
+        default: throw Error(E_ARG, "unknown interpolation method");
+    }
+    FRG_CHECK_LAUNCH();
+}
+
+}  // namespace frg

@@ -54,6 +54,8 @@ PlanCache::~PlanCache() {
 
 static PlanCache g_plans;
 
+PlanCache& shared_plans() { return g_plans; }
+
 Workspace::~Workspace() {}
 void* Workspace::get(size_t bytes) {
     if (bytes > cap) {
@@ -129,12 +131,20 @@ struct Bin {
     bool nyq[3];  // |m| == n/2 (for n > 1)
 };
 
-__device__ __forceinline__ Bin bin_of(const Dims& g, long long p) {
-    int nh = g.n2 / 2 + 1;
-    int i2 = (int)(p % nh);
-    long long r = p / nh;
-    int i1 = (int)(r % g.n1);
-    int i0 = (int)(r / g.n1);
+// half-spectrum launch geometry: block (32, 8) over (i2, i1), grid z over i0
+inline dim3 spec_grid(const Dims& g) { return dim3((g.n2 / 2 + 1 + BX - 1) / BX, (g.n1 + BY - 1) / BY, g.n0); }
+
+__device__ __forceinline__ bool spec_vox(const Dims& g, int& i0, int& i1, int& i2, int& p) {
+    const int nh = g.n2 / 2 + 1;
+    i2 = blockIdx.x * BX + threadIdx.x;
+    i1 = blockIdx.y * BY + threadIdx.y;
+    i0 = blockIdx.z;
+    if (i2 >= nh || i1 >= g.n1) return false;
+    p = (i0 * g.n1 + i1) * nh + i2;
+    return true;
+}
+
+__device__ __forceinline__ Bin bin_of(const Dims& g, int i0, int i1, int i2) {
     Bin b;
     int f0 = dft_freq(i0, g.n0), f1 = dft_freq(i1, g.n1);
     int f2 = (i2 == g.n2 / 2) ? -(g.n2 / 2) : i2;
@@ -220,9 +230,9 @@ struct CR<cufftDoubleComplex> {
 
 template <typename C>
 __global__ void k_spec_scale(Dims g, long long nh, int ncomp, C* __restrict__ x, int kind, RegSpec r, double invN) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nh) return;
-    Bin b = bin_of(g, p);
+    int i0, i1, i2, p;
+    if (!spec_vox(g, i0, i1, i2, p)) return;
+    Bin b = bin_of(g, i0, i1, i2);
     double s = symbol_of(g, b, kind, r) * invN;
     using R = typename CR<C>::R;
     for (int c = 0; c < ncomp; ++c) {
@@ -238,9 +248,9 @@ __global__ void k_spec_scale(Dims g, long long nh, int ncomp, C* __restrict__ x,
 template <typename CA, typename CB>
 __global__ void k_spec_combine(Dims g, long long nh, CA* __restrict__ a, const CB* __restrict__ bsp, RegSpec r,
                                double invN, bool have_a, bool project) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nh) return;
-    Bin bn = bin_of(g, p);
+    int i0, i1, i2, p;
+    if (!spec_vox(g, i0, i1, i2, p)) return;
+    Bin bn = bin_of(g, i0, i1, i2);
     double ksq = bn.m[0] * bn.m[0] + bn.m[1] * bn.m[1] + bn.m[2] * bn.m[2];
     double sa = have_a ? r.alpha * reg_sym(ksq, r) * invN : 0.0;
     double br[3], bi[3], k[3] = {0, 0, 0}, mfac = 0.0;
@@ -276,9 +286,9 @@ __global__ void k_spec_combine(Dims g, long long nh, CA* __restrict__ a, const C
 // spectral gradient of a scalar: out_c = -i m_axis(c) u  (Nyquist zeroed), diffops.py:56-73
 template <typename C>
 __global__ void k_spec_grad(Dims g, long long nh, const C* __restrict__ u, C* __restrict__ out, double invN) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nh) return;
-    Bin b = bin_of(g, p);
+    int i0, i1, i2, p;
+    if (!spec_vox(g, i0, i1, i2, p)) return;
+    Bin b = bin_of(g, i0, i1, i2);
     C v = u[p];
     using R = typename CR<C>::R;
     for (int c = 0; c < g.d; ++c) {
@@ -294,9 +304,9 @@ __global__ void k_spec_grad(Dims g, long long nh, const C* __restrict__ u, C* __
 
 template <typename C>
 __global__ void k_spec_div(Dims g, long long nh, const C* __restrict__ v, C* __restrict__ out, double invN) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nh) return;
-    Bin b = bin_of(g, p);
+    int i0, i1, i2, p;
+    if (!spec_vox(g, i0, i1, i2, p)) return;
+    Bin b = bin_of(g, i0, i1, i2);
     double orr = 0.0, oi = 0.0;
     for (int c = 0; c < g.d; ++c) {
         int a = g.comp_axis(c);
@@ -315,11 +325,9 @@ __global__ void k_spec_div(Dims g, long long nh, const C* __restrict__ v, C* __r
 // Parseval: per-bin weight (1 on the i2 = 0 and i2 = n2/2 planes, else 2)
 template <typename C>
 __global__ void k_spec_energy(Dims g, long long nh, const C* __restrict__ v, RegSpec r, double* __restrict__ out) {
-    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nh) return;
-    Bin b = bin_of(g, p);
-    int nhz = g.n2 / 2 + 1;
-    int i2 = (int)(p % nhz);
+    int i0, i1, i2, p;
+    if (!spec_vox(g, i0, i1, i2, p)) return;
+    Bin b = bin_of(g, i0, i1, i2);
     double w = (i2 == 0 || i2 == g.n2 / 2) ? 1.0 : 2.0;
     double ksq = b.m[0] * b.m[0] + b.m[1] * b.m[1] + b.m[2] * b.m[2];
     double s = r.alpha * reg_sym(ksq, r);
@@ -407,7 +415,7 @@ static void spectral_apply_t(PlanCache& pc, void* ws, const Dims& g, int ncomp, 
     long long nh = half_len(g);
     C* sp = (C*)ws;
     fwd<R>(pc, g, ncomp, in, sp, st);
-    k_spec_scale<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ncomp, sp, kind, r, 1.0 / (double)g.N);
+    k_spec_scale<C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, ncomp, sp, kind, r, 1.0 / (double)g.N);
     FRG_CHECK_LAUNCH();
     inv<R>(pc, g, ncomp, sp, out, st);
 }
@@ -441,7 +449,7 @@ static void combine_t(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, cons
     CB* sb = (CB*)ws_b;
     if (a) fwd<RA>(pc, g, g.d, a, sa, st);
     fwd<RB>(pc, g, g.d, b, sb, st);
-    k_spec_combine<CA, CB><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, sa, sb, r, 1.0 / (double)g.N, a != nullptr,
+    k_spec_combine<CA, CB><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, sa, sb, r, 1.0 / (double)g.N, a != nullptr,
                                                                      project_on);
     FRG_CHECK_LAUNCH();
     inv<RA>(pc, g, g.d, sa, out, st);
@@ -477,7 +485,7 @@ void project(const Dims& g, int dtype, const void* b, void* out, const RegSpec& 
         using C = cufftDoubleComplex;
         long long nh = half_len(g);
         fwd<double>(g_plans, g, g.d, (const double*)b, (C*)ws, st);
-        k_spec_combine<C, C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
+        k_spec_combine<C, C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
                                                                        1.0 / (double)g.N, false, true);
         FRG_CHECK_LAUNCH();
         inv<double>(g_plans, g, g.d, (C*)ws, (double*)out, st);
@@ -485,7 +493,7 @@ void project(const Dims& g, int dtype, const void* b, void* out, const RegSpec& 
         using C = cufftComplex;
         long long nh = half_len(g);
         fwd<float>(g_plans, g, g.d, (const float*)b, (C*)ws, st);
-        k_spec_combine<C, C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
+        k_spec_combine<C, C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, (C*)ws, (const C*)ws, r,
                                                                        1.0 / (double)g.N, false, true);
         FRG_CHECK_LAUNCH();
         inv<float>(g_plans, g, g.d, (C*)ws, (float*)out, st);
@@ -499,7 +507,7 @@ static void spec_grad_t(const Dims& g, const R* u, R* out, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_ws_mu);
     C* ws = (C*)g_ws.get(sizeof(C) * nh * (g.d + 1));
     fwd<R>(g_plans, g, 1, u, ws, st);
-    k_spec_grad<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, ws + nh, 1.0 / (double)g.N);
+    k_spec_grad<C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, ws, ws + nh, 1.0 / (double)g.N);
     FRG_CHECK_LAUNCH();
     inv<R>(g_plans, g, g.d, ws + nh, out, st);
 }
@@ -518,7 +526,7 @@ static void spec_div_t(const Dims& g, const R* v, R* out, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_ws_mu);
     C* ws = (C*)g_ws.get(sizeof(C) * nh * (g.d + 1));
     fwd<R>(g_plans, g, g.d, v, ws, st);
-    k_spec_div<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, ws + (long long)g.d * nh, 1.0 / (double)g.N);
+    k_spec_div<C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, ws, ws + (long long)g.d * nh, 1.0 / (double)g.N);
     FRG_CHECK_LAUNCH();
     inv<R>(g_plans, g, 1, ws + (long long)g.d * nh, out, st);
 }
@@ -537,7 +545,7 @@ static double reg_energy_t(PlanCache& pc, void* wsv, const Dims& g, const R* v, 
     C* ws = (C*)wsv;
     double* vals = (double*)(ws + (long long)g.d * nh);
     fwd<R>(pc, g, g.d, v, ws, st);
-    k_spec_energy<C><<<blocks_for(nh, S_TPB), S_TPB, 0, st>>>(g, nh, ws, r, vals);
+    k_spec_energy<C><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, ws, r, vals);
     FRG_CHECK_LAUNCH();
     double mms[3];
     min_max_sum(F64, vals, nh, mms, st);

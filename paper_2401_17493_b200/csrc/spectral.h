@@ -27,6 +27,8 @@ struct Workspace {
     ~Workspace();
 };
 
+// process-wide plan cache (plans are keyed by shape/type/batch; the stream is set per call)
+PlanCache& shared_plans();
 long long half_len(const Dims& g);
 Dims coarse_dims(const Dims& gf);
 size_t spectral_ws_bytes(const Dims& g, int dtype, int ncomp);
