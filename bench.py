@@ -260,17 +260,21 @@ def run_b200(a):
         del st
         torch.cuda.synchronize()
         barrier()
-        F.register(m0, m1, reg=reg, precond=F.PrecondKind("reg"), method="cubic", scheme="fd8",
-                   transport_dtype=tdt, config=F.OptimizerConfig(max_outer=1))  # warm plans
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        vsol, rep = F.register(m0, m1, reg=reg, precond=F.PrecondKind("reg"), method="cubic", scheme="fd8",
-                               transport_dtype=tdt)
-        torch.cuda.synchronize()
-        wall = max_over_ranks(time.perf_counter() - t0)
-        tts = {"seconds": wall, "iterations": rep.iterations, "matvecs": rep.matvecs, "pde_solves": rep.pde_solves,
-               "status": rep.status, "mismatch": rep.mismatch, "gradient": rep.gradient, "precond": "reg",
-               "detgrad_min": rep.detgrad_min}
+        # one untimed solve creates the cuFFT plans (process-wide cache), then two timed solves
+        walls = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            vsol, rep = F.register(m0, m1, reg=reg, precond=F.PrecondKind("reg"), method="cubic", scheme="fd8",
+                                   transport_dtype=tdt)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        wall = max_over_ranks(min(walls[1:]))
+        tts = {"seconds": wall, "first_call_seconds": walls[0], "iterations": rep.iterations,
+               "matvecs": rep.matvecs, "pde_solves": rep.pde_solves, "status": rep.status, "mismatch": rep.mismatch,
+               "gradient": rep.gradient, "precond": "reg", "detgrad_min": rep.detgrad_min,
+               "includes": "KktState creation, all refresh/gradient/PCG/Armijo work and det(F) stats; "
+                           "excludes synthetic-data generation"}
 
     if world > 1:
         dist.barrier()

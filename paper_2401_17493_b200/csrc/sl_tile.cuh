@@ -159,6 +159,27 @@ __device__ __forceinline__ void stage_box(T* __restrict__ box, const V* __restri
     }
 }
 
+// 16-byte chunked staging (cp.async.cg 16 B): rows of the box are whole
+// aligned chunks inside the period along k; one (row, chunk) per thread.
+template <typename T>
+__device__ __forceinline__ void stage_box_vec(T* __restrict__ box, const T* __restrict__ src, const Dims& g, int lo0,
+                                              int lo1, int lo2, int S0, int S1, int S2c, int S2p, int tid) {
+    constexpr int VEC = 16 / (int)sizeof(T);
+    const unsigned mc = div_magic((unsigned)S2c), m1 = div_magic((unsigned)S1);
+    const int total = S0 * S1 * S2c;
+    for (int q = tid; q < total; q += BX * BY) {
+        const int r = (int)fast_div((unsigned)q, mc);
+        const int ch = q - r * S2c;
+        const int a = (int)fast_div((unsigned)r, m1);
+        const int b = r - a * S1;
+        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1);
+        const T* s = src + ((gi * g.n1 + gj) * g.n2 + lo2 + ch * VEC);
+        unsigned d = (unsigned)__cvta_generic_to_shared(box + (r * S2p + ch * VEC));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(s));
+    }
+    cp_async_wait_all();
+}
+
 template <int M>
 struct Halo {
     static constexpr int lo = (M == CUBIC ? 1 : 0);
@@ -297,10 +318,25 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) 
         mx2 = max(mx2, red[5][w]);
     }
     if (mn0 == INT_MAX) return;  // empty tile (uniform across the CTA)
-    const int lo0 = mn0 - Halo<M>::lo, lo1 = mn1 - Halo<M>::lo, lo2 = mn2 - Halo<M>::lo;
+    const int lo0 = mn0 - Halo<M>::lo, lo1 = mn1 - Halo<M>::lo;
+    int lo2 = mn2 - Halo<M>::lo;
     const int S0 = mx0 + Halo<M>::hi - lo0 + 1;
     const int S1 = mx1 + Halo<M>::hi - lo1 + 1;
-    const int S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    int S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    // 16-byte staging: widen the k-range to whole 16-byte chunks when the rows
+    // need no periodic wrap along k (the common case)
+    constexpr int VEC = 16 / (int)sizeof(T);
+    bool vec = sizeof(T) == sizeof(typename Op::V) && (g.n2 % VEC) == 0 && lo2 >= 0;
+    if (vec) {
+        const int a2 = lo2 - lo2 % VEC;
+        const int w = ((S2 + (lo2 - a2) + VEC - 1) / VEC) * VEC;
+        if (a2 + w <= g.n2) {
+            lo2 = a2;
+            S2 = w;
+        } else {
+            vec = false;
+        }
+    }
     // rows padded to 32 elements: lanes of a warp on different box rows then
     // never hit the same shared-memory bank (their columns differ by < 32)
     const int S2p = (S2 + 31) & ~31;
@@ -313,7 +349,11 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) 
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             if (f > 0) __syncthreads();
-            stage_box<T, typename Op::V>(box, op.field(f), g, lo0, lo1, lo2, S1, S2, S2p, (int)vol, tid);
+            const typename Op::V* src = op.field(f);
+            if (vec && (((uintptr_t)src & 15) == 0))
+                stage_box_vec<T>(box, (const T*)src, g, lo0, lo1, lo2, S0, S1, S2 / VEC, S2p, tid);
+            else
+                stage_box<T, typename Op::V>(box, src, g, lo0, lo1, lo2, S1, S2, S2p, (int)vol, tid);
             __syncthreads();
             if constexpr (FRG_SL_PAIRED && M == CUBIC && sizeof(T) == 4 && SL_TI % 2 == 0) {
                 // paired FFMA2 evaluation; an inactive partner reuses its twin's taps
