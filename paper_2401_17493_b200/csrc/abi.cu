@@ -141,10 +141,10 @@ int frg_solve_inc_state(const int32_t n[3], int32_t d, int32_t dtype, int32_t vd
         cudaStream_t st = ST(stream);
         char* work = nullptr;
         size_t per = (size_t)g.d * g.N * T;
-        FRG_CUDA(cudaMallocAsync((void**)&work, per * (n_t + 2), st));
+        FRG_CUDA(cudaMallocAsync((void**)&work, per * (n_t + 1) + (size_t)(n_t > 1 ? n_t - 1 : 1) * g.N * T, st));
         void* grads_y = work;
         void* vtT = work + per * n_t;
-        void* vty = work + per * (n_t + 1);
+        void* S = work + per * (n_t + 1);
         std::vector<const void*> in(g.d * n_t);
         std::vector<void*> out(g.d * n_t);
         for (long long e = 0; e < (long long)g.d * n_t; ++e) {
@@ -152,7 +152,7 @@ int frg_solve_inc_state(const int32_t n[3], int32_t d, int32_t dtype, int32_t vd
             out[e] = work + e * g.N * T;
         }
         gather_fields(g, dtype, method, disp, g.d * n_t, in.data(), out.data(), st);
-        inc_state(g, dtype, vdtype, method, n_t, disp, grads, grads_y, vt, vtT, vty, series, nullptr, 0.0, true, st);
+        inc_state(g, dtype, vdtype, method, n_t, disp, grads, grads_y, vt, vtT, S, series, nullptr, 0.0, true, st);
         FRG_CUDA(cudaFreeAsync(work, st));
     });
 }

@@ -104,7 +104,7 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
     k->grads_y.alloc(n_t * d * N * T);
     k->lam.alloc((n_t + 1) * N * T);
     k->vtT.alloc(d * N * T);
-    k->vty.alloc(d * N * T);
+    k->vty.alloc((n_t > 1 ? n_t - 1 : 1) * N * T);  // incremental-state Heun sources S_1..S_{n_t-1}
     k->mt.alloc(2 * N * T);
     k->lt.alloc((n_t + 1) * N * T);
     k->bf.alloc(d * N * T);

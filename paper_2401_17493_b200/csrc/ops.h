@@ -36,11 +36,12 @@ void adjoint_step(const Dims& g, int tdtype, int method, const void* disp_b, con
 void solve_adjoint(const Dims& g, int tdtype, int method, int n_t, const void* disp_b,
                    const void* cmul, void* series, cudaStream_t st);
 // incremental state. grads: (n_t+1) x d x N at x; grads_y: n_t x d x N gathered at y.
-// vt: control dtype. Writes vty/vtT (d x N each, tdtype) and the series slices
+// vt: control dtype. Writes vtT (d x N, tdtype), the Heun sources S ((n_t-1) x N,
+// tdtype) and the series slices
 // (n_t+1) x N (slice 0 zeroed); if final_sign != 0 and final_out != nullptr the
 // last slice is also written as final_sign * m~(1) into final_out.
 void inc_state(const Dims& g, int tdtype, int cdtype, int method, int n_t, const void* disp,
-               const void* grads, const void* grads_y, const void* vt, void* vtT, void* vty,
+               const void* grads, const void* grads_y, const void* vt, void* vtT, void* S,
                void* series, void* final_out, double final_sign, bool keep_series,
                cudaStream_t st);
 // trapezoid body force b = sum_j w_j lam_j grad_j, written in odtype; if

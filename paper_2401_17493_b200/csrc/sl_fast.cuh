@@ -1,0 +1,440 @@
+// TMA-staged fp32 semi-Lagrangian gather engine (sm_100a).
+//
+// Same contract as k_sl (sl_tile.cuh: Op supplies disp / field / done), for
+// fp32 fields gathered with LINEAR or CUBIC stencils — every fp32 SL step of
+// the state, adjoint, incremental and departure solves.  Differences:
+//
+//  * the shared-memory box has a FIXED geometry TB_I x TB_J x TB_K (planes x
+//    rows x columns), so every tap of a stencil is one LDS at a compile-time
+//    immediate offset from a single per-voxel base address (no per-row
+//    address arithmetic: 64 LDS + 84 FMA per cubic point);
+//  * the box is filled by TMA (cp.async.bulk.tensor.2d over the field viewed
+//    as (n0*n1) rows x n2 columns, one TB_J x TB_K load per needed plane,
+//    issued by one thread and completed on an mbarrier): no per-element
+//    staging instructions in the SM.  Periodic wrap: planes wrap exactly
+//    (the plane index is reduced before the load); rows / columns leaving
+//    the grid are patched with 4-byte cp.async from their periodic images
+//    after the TMA lands.  Grids smaller than the box (tests, 2D) stage the
+//    whole box with cp.async instead.  (per-plane 2D loads let the plane index
+//    wrap exactly and load only the S0 planes a tile needs);
+//  * multi-field gathers reuse the box: the TMA of field f+1 is issued as
+//    soon as field f has been consumed;
+//  * tiles whose stencil bounding box exceeds the fixed box gather straight
+//    from global memory (any displacement field is handled).
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdlib>
+#include <type_traits>
+
+#include "sl_tile.cuh"
+
+namespace frg {
+
+// box: 64 x 16 x 12 fp32 = 48 KB.  TMA box starts must be 16-byte aligned
+// along the contiguous axis (an unaligned start faults with an illegal
+// instruction), so the column origin is rounded down to a multiple of 4.
+// Row pitch 64 (= 0 mod 32 banks): lanes of a warp whose stencils sit on
+// different box rows still hit distinct banks (their columns differ).
+constexpr int TB_K = 64, TB_J = 16, TB_I = 12;
+constexpr int TB_VOL = TB_K * TB_J * TB_I;
+constexpr int TB_PLANE = TB_K * TB_J;
+
+template <int NF>
+struct alignas(64) TmaMaps {
+    CUtensorMap m[NF];
+};
+
+// host: 2D tiled tensor map over an fp32 (n0, n1, n2) field viewed as
+// (n0*n1, n2), box TB_J rows x TB_K columns
+void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g);
+// host: whether the TMA engine applies to this grid (every axis >= its box edge)
+inline bool tma_grid_ok(const Dims& g) { return g.n0 >= TB_I && g.n1 >= TB_J && g.n2 >= TB_K && (g.n2 % 4) == 0; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(float* dst, const CUtensorMap* map, int col, int row, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_u32(dst)),
+        "l"((unsigned long long)map), "r"(col), "r"(row), "r"(smem_u32(bar))
+        : "memory");
+}
+// issue the S0 plane loads of one field box (one thread)
+__device__ __forceinline__ void tma_box(float* box, const CUtensorMap* map, const Dims& g, int lo0, int lo1, int lo2,
+                                        int S0, uint64_t* bar) {
+    mbar_expect_tx(bar, (unsigned)(S0 * TB_PLANE * sizeof(float)));
+    for (int a = 0; a < S0; ++a) tma_load_2d(box + a * TB_PLANE, map, lo2, wrap_near(lo0 + a, g.n0) * g.n1 + lo1, bar);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Lagrange cubic weights (nodes -1, 0, 1, 2; _kernels.py:162-167) in 3 FADD +
+// 10 FMUL: the shared products t(t-1) and (t+1)(t-2) are formed once.
+__device__ __forceinline__ void lagrange4f(float t, float (&w)[4]) {
+    const float tm1 = t - 1.f, tm2 = t - 2.f, tp1 = t + 1.f;
+    const float p = t * tm1, q = tp1 * tm2;
+    w[0] = (p * tm2) * (-1.f / 6.f);
+    w[1] = (q * tm1) * 0.5f;
+    w[2] = (q * t) * -0.5f;
+    w[3] = (p * tp1) * (1.f / 6.f);
+}
+
+// 64-tap cubic from a fixed-geometry box: every tap an immediate offset from p
+__device__ __forceinline__ float cubic_fixed(const float* __restrict__ p, const float (&w0)[4], const float (&w1)[4],
+                                             const float (&w2)[4]) {
+    float acc = 0.f;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        float plane = 0.f;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const float* row = p + a * TB_PLANE + b * TB_K;
+            float r = w2[0] * row[0];
+            r = fmaf(w2[1], row[1], r);
+            r = fmaf(w2[2], row[2], r);
+            r = fmaf(w2[3], row[3], r);
+            plane = fmaf(w1[b], r, plane);
+        }
+        acc = fmaf(w0[a], plane, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ float linear_fixed(const float* __restrict__ b, float t0, float t1, float t2) {
+    // same expression order as box_interp<LINEAR> / apply_stencil<LINEAR>
+    float c00 = (1.f - t2) * b[0] + t2 * b[1];
+    float c01 = (1.f - t2) * b[TB_K] + t2 * b[TB_K + 1];
+    float c10 = (1.f - t2) * b[TB_PLANE] + t2 * b[TB_PLANE + 1];
+    float c11 = (1.f - t2) * b[TB_PLANE + TB_K] + t2 * b[TB_PLANE + TB_K + 1];
+    return (1.f - t0) * ((1.f - t1) * c00 + t1 * c01) + t0 * ((1.f - t1) * c10 + t1 * c11);
+}
+
+// copy the box elements whose coordinate along `axis` leaves [0, n) from their
+// periodic images (after the TMA zero-filled them); 4-byte cp.async
+__device__ __forceinline__ void patch_axis(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
+                                           int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid) {
+    const int lo = axis == 0 ? lo0 : (axis == 1 ? lo1 : lo2);
+    const int S = axis == 0 ? S0 : (axis == 1 ? S1 : S2);
+    const int n = g.axis_len(axis);
+    // out-of-range index ranges along the axis: [0, a_end) and [b_beg, S)
+    const int a_end = lo < 0 ? min(-lo, S) : 0;
+    const int b_beg = lo + S > n ? max(n - lo, 0) : S;
+    const int cnt = a_end + (S - b_beg);
+    if (cnt == 0) return;
+    // the two other extents
+    const int E1 = axis == 0 ? S1 : S0;           // outer of the remaining pair
+    const int E2 = axis == 2 ? S1 : S2;           // inner of the remaining pair
+    const int total = cnt * E1 * E2;
+    for (int e = tid; e < total; e += BX * BY) {
+        int r = e / E2;
+        const int in2 = e - r * E2;
+        const int q = r / E1;
+        const int in1 = r - q * E1;
+        const int x = q < a_end ? q : b_beg + (q - a_end);
+        int a, b, c;
+        if (axis == 0) {
+            a = x; b = in1; c = in2;
+        } else if (axis == 1) {
+            a = in1; b = x; c = in2;
+        } else {
+            a = in1; b = in2; c = x;
+        }
+        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        cp_async_elem<4>(box + (a * TB_J + b) * TB_K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
+    }
+}
+
+// whole-box cp.async staging with wrap (grids smaller than the TMA box)
+__device__ __forceinline__ void stage_fixed(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
+                                            int lo0, int lo1, int lo2, int S0, int S1, int S2, int tid) {
+    const int total = S0 * S1 * S2;
+    for (int e = tid; e < total; e += BX * BY) {
+        int r = e / S2;
+        const int c = e - r * S2;
+        const int a = r / S1;
+        const int b = r - a * S1;
+        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        cp_async_elem<4>(box + (a * TB_J + b) * TB_K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
+    }
+}
+
+template <int NF>
+struct SlfSmem {
+    static constexpr int NB = 1;  // one 48 KB box per CTA (4 CTAs / SM)
+    // + 1 KB: the dynamic window is re-aligned to 1024 B in the kernel (the
+    // compiler-placed start after the static shared variables is not)
+    static constexpr size_t bytes = (size_t)NB * TB_VOL * sizeof(float) + 1024;
+};
+
+template <class Op, class = void>
+struct PreOf {
+    struct type {};
+};
+template <class Op>
+struct PreOf<Op, std::void_t<typename Op::Pre>> {
+    using type = typename Op::Pre;
+};
+
+// Lagrange weights for two points at once (Blackwell paired fp32: FADD2/FMUL2),
+// lane-for-lane identical to lagrange4f
+__device__ __forceinline__ void lagrange4f_x2(float2 t, float2 (&w)[4]) {
+    const float2 tm1 = __fadd2_rn(t, make_float2(-1.f, -1.f)), tm2 = __fadd2_rn(t, make_float2(-2.f, -2.f));
+    const float2 tp1 = __fadd2_rn(t, make_float2(1.f, 1.f));
+    const float2 p = __fmul2_rn(t, tm1), q = __fmul2_rn(tp1, tm2);
+    w[0] = __fmul2_rn(__fmul2_rn(p, tm2), make_float2(-1.f / 6.f, -1.f / 6.f));
+    w[1] = __fmul2_rn(__fmul2_rn(q, tm1), make_float2(0.5f, 0.5f));
+    w[2] = __fmul2_rn(__fmul2_rn(q, t), make_float2(-0.5f, -0.5f));
+    w[3] = __fmul2_rn(__fmul2_rn(p, tp1), make_float2(1.f / 6.f, 1.f / 6.f));
+}
+
+// two cubic stencils with paired FMAs: the taps of point A and point B load
+// into the two halves of one register pair; lane-for-lane identical to
+// cubic_fixed
+__device__ __forceinline__ float2 cubic_fixed_x2(const float* __restrict__ pA, const float* __restrict__ pB,
+                                                 const float2 (&w0)[4], const float2 (&w1)[4],
+                                                 const float2 (&w2)[4]) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        float2 plane = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const float* rA = pA + a * TB_PLANE + b * TB_K;
+            const float* rB = pB + a * TB_PLANE + b * TB_K;
+            float2 r = __fmul2_rn(w2[0], make_float2(rA[0], rB[0]));
+            r = __ffma2_rn(w2[1], make_float2(rA[1], rB[1]), r);
+            r = __ffma2_rn(w2[2], make_float2(rA[2], rB[2]), r);
+            r = __ffma2_rn(w2[3], make_float2(rA[3], rB[3]), r);
+            plane = __ffma2_rn(w1[b], r, plane);
+        }
+        acc = __ffma2_rn(w0[a], plane, acc);
+    }
+    return acc;
+}
+
+// mbarrier wait with a suspend-time hint: the warp sleeps in hardware until
+// the phase completes instead of spinning on try_wait (issue slots stay free)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n"
+        "@!P1 bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int M, int NF, class Op>
+__global__ void __launch_bounds__(BX* BY, 4)
+    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
+    static_assert(M == LINEAR || M == CUBIC, "k_slf: linear / cubic only");
+    static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
+    extern __shared__ __align__(16) unsigned char sdyn[];
+    // offset arithmetic on the shared array itself (not through uintptr_t) so
+    // that the taps compile to LDS, not generic LD
+    float* sbox = reinterpret_cast<float*>(sdyn + ((1024u - (smem_u32(sdyn) & 1023u)) & 1023u));
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int bb[6];  // min0, min1, min2, -max0, -max1, -max2 of the stencil bases
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+    const int k = blockIdx.x * BX + tx;
+    const int j = blockIdx.y * BY + ty;
+    const int i_base = blockIdx.z * SL_TI;
+    const bool in_kj = (k < g.n2) && (j < g.n1);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (tid < 6) bb[tid] = INT_MAX;
+
+    int base0[SL_TI], base1[SL_TI], base2[SL_TI];
+    float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
+    bool ok[SL_TI];
+    int mn0 = INT_MAX, mn1 = INT_MAX, mn2 = INT_MAX, mx0 = INT_MIN, mx1 = INT_MIN, mx2 = INT_MIN;
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const int i = i_base + u;
+        ok[u] = in_kj && i < g.n0;
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+        if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, d0, d1, d2);
+        const float f0 = floorf(d0), f1 = floorf(d1), f2 = floorf(d2);
+        base0[u] = i + (int)f0;
+        base1[u] = j + (int)f1;
+        base2[u] = k + (int)f2;
+        fr0[u] = d0 - f0;
+        fr1[u] = d1 - f1;
+        fr2[u] = d2 - f2;
+        if (ok[u]) {
+            mn0 = min(mn0, base0[u]);
+            mx0 = max(mx0, base0[u]);
+            mn1 = min(mn1, base1[u]);
+            mx1 = max(mx1, base1[u]);
+            mn2 = min(mn2, base2[u]);
+            mx2 = max(mx2, base2[u]);
+        }
+    }
+    // CTA bounding box: warp REDUX, then 6 shared atomics per warp
+    mn0 = warp_min_i(mn0);
+    mn1 = warp_min_i(mn1);
+    mn2 = warp_min_i(mn2);
+    mx0 = warp_max_i(mx0);
+    mx1 = warp_max_i(mx1);
+    mx2 = warp_max_i(mx2);
+    __syncthreads();  // bb initialised
+    if (tx == 0 && mn0 != INT_MAX) {
+        atomicMin(&bb[0], mn0);
+        atomicMin(&bb[1], mn1);
+        atomicMin(&bb[2], mn2);
+        atomicMin(&bb[3], -mx0);
+        atomicMin(&bb[4], -mx1);
+        atomicMin(&bb[5], -mx2);
+    }
+    __syncthreads();
+    mn0 = bb[0];
+    if (mn0 == INT_MAX) return;  // empty tile (uniform across the CTA)
+    mn1 = bb[1];
+    mn2 = bb[2];
+    mx0 = -bb[3];
+    mx1 = -bb[4];
+    mx2 = -bb[5];
+    const int lo0 = mn0 - Halo<M>::lo, lo1 = mn1 - Halo<M>::lo, lo2 = (mn2 - Halo<M>::lo) & ~3;
+    const int S0 = mx0 + Halo<M>::hi - lo0 + 1;
+    const int S1 = mx1 + Halo<M>::hi - lo1 + 1;
+    const int S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
+    if (fits && use_tma && tid == 0) tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
+
+    // epilogue inputs: loads in flight while the box lands and the stencils run
+    using PreT = typename PreOf<Op>::type;
+    PreT pre[SL_TI];
+    if constexpr (HasPre<Op>::value) {
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u)
+            if (ok[u]) pre[u] = op.pre(((i_base + u) * g.n1 + j) * g.n2 + k);
+    }
+
+    float vals[SL_TI][NF];
+    if (fits) {
+        const bool wrap = lo0 < 0 || lo0 + S0 > g.n0 || lo1 < 0 || lo1 + S1 > g.n1 || lo2 < 0 || lo2 + S2 > g.n2;
+        // per-voxel smem offset of the first tap (same for every field)
+        int off[SL_TI];
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u)  // inactive voxels read tap 0 (result discarded)
+            off[u] = ok[u] ? ((base0[u] - Halo<M>::lo - lo0) * TB_J + (base1[u] - Halo<M>::lo - lo1)) * TB_K +
+                                 (base2[u] - Halo<M>::lo - lo2)
+                           : 0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const float* src = op.field(f);
+            if (use_tma) {
+                mbar_wait_sleep(&bar, (unsigned)(f & 1));
+                if (wrap) {  // planes already wrapped by tma_box
+                    patch_axis(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
+                    patch_axis(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
+                    cp_async_wait_all();
+                    __syncthreads();
+                }
+            } else {
+                if (f > 0) __syncthreads();
+                stage_fixed(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, tid);
+                cp_async_wait_all();
+                __syncthreads();
+            }
+            if (M == CUBIC) {
+#pragma unroll
+                for (int u = 0; u < SL_TI; u += 2) {
+                    float2 w0[4], w1[4], w2[4];
+                    lagrange4f_x2(make_float2(fr0[u], fr0[u + 1]), w0);
+                    lagrange4f_x2(make_float2(fr1[u], fr1[u + 1]), w1);
+                    lagrange4f_x2(make_float2(fr2[u], fr2[u + 1]), w2);
+                    const float2 r = cubic_fixed_x2(sbox + off[u], sbox + off[u + 1], w0, w1, w2);
+                    vals[u][f] = r.x;
+                    vals[u + 1][f] = r.y;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < SL_TI; ++u) vals[u][f] = linear_fixed(sbox + off[u], fr0[u], fr1[u], fr2[u]);
+            }
+            if (use_tma && f + 1 < NF) {
+                __syncthreads();  // every thread is done reading the box
+                if (tid == 0) {
+                    fence_proxy_async();
+                    tma_box(sbox, &maps.m[f + 1], g, lo0, lo1, lo2, S0, &bar);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const float* src = op.field(f);
+#pragma unroll
+            for (int u = 0; u < SL_TI; ++u)
+                vals[u][f] = ok[u] ? global_interp<float, M, float>(g, src, base0[u], base1[u], base2[u], fr0[u],
+                                                                    fr1[u], fr2[u])
+                                   : 0.f;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u)
+        if (ok[u]) {
+            const int p = ((i_base + u) * g.n1 + j) * g.n2 + k;
+            if constexpr (HasPre<Op>::value)
+                op.done(p, vals[u], pre[u]);
+            else
+                op.done(p, vals[u]);
+        }
+}
+
+template <int M, int NF, class Op>
+void launch_slf(const Dims& g, const Op& op, cudaStream_t st) {
+    TmaMaps<NF> maps;
+    const int use_tma = tma_grid_ok(g) ? 1 : 0;
+    for (int f = 0; f < NF; ++f) {
+        if (use_tma)
+            encode_field_map(&maps.m[f], op.field(f), g);
+        else
+            memset(&maps.m[f], 0, sizeof(CUtensorMap));
+    }
+    constexpr size_t smem = SlfSmem<NF>::bytes;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        FRG_CUDA(cudaFuncSetAttribute(k_slf<M, NF, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    k_slf<M, NF, Op><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma);
+    FRG_CHECK_LAUNCH();
+}
+
+// Every SL launch: fp32 linear / cubic gathers of fp32 fields take the TMA
+// engine, everything else (f64 parity path, nearest, converting sources) the
+// generic staged engine of sl_tile.cuh.
+template <typename T, int NF, class Op>
+void launch_sl(const Dims& g, int method, const Op& op, cudaStream_t st) {
+    if constexpr (std::is_same<T, float>::value && std::is_same<typename Op::V, float>::value) {
+        if (method == CUBIC) return launch_slf<CUBIC, NF, Op>(g, op, st);
+        if (method == LINEAR) return launch_slf<LINEAR, NF, Op>(g, op, st);
+    }
+    launch_sl_generic<T, NF, Op>(g, method, op, st);
+}
+
+}  // namespace frg

@@ -19,6 +19,8 @@
 #pragma once
 
 #include <climits>
+#include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 
@@ -178,6 +180,22 @@ __device__ __forceinline__ void stage_box_vec(T* __restrict__ box, const T* __re
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(s));
     }
     cp_async_wait_all();
+}
+
+// Ops may split their epilogue into a load phase (pre(p) -> Op::Pre, issued
+// before the stencils are evaluated, so its latency hides behind them) and a
+// compute/store phase (done(p, vals, pre)).  Ops without pre() get done(p, vals).
+template <class Op, class = void>
+struct HasPre : std::false_type {};
+template <class Op>
+struct HasPre<Op, std::void_t<decltype(std::declval<const Op&>().pre(0))>> : std::true_type {};
+
+template <class Op, typename T, int NF>
+__device__ __forceinline__ void op_done(const Op& op, int p, const T (&vals)[NF]) {
+    if constexpr (HasPre<Op>::value)
+        op.done(p, vals, op.pre(p));
+    else
+        op.done(p, vals);
 }
 
 template <int M>
@@ -398,7 +416,7 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) 
 #pragma unroll
     for (int u = 0; u < SL_TI; ++u) {
         const int i = i_base + u;
-        if (in_kj && i < g.n0) op.done((i * g.n1 + j) * g.n2 + k, vals[u]);
+        if (in_kj && i < g.n0) op_done(op, (i * g.n1 + j) * g.n2 + k, vals[u]);
     }
 }
 
@@ -432,7 +450,7 @@ inline dim3 sl_grid(const Dims& g) {
 }
 
 template <typename T, int NF, class Op>
-void launch_sl(const Dims& g, int method, const Op& op, cudaStream_t st) {
+void launch_sl_generic(const Dims& g, int method, const Op& op, cudaStream_t st) {
     switch (method) {
         case NEAREST: k_sl<T, NEAREST, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
         case LINEAR: k_sl<T, LINEAR, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;

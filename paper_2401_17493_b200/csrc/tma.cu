@@ -1,0 +1,38 @@
+// Host-side TMA descriptors for the SL engine (sl_fast.cuh).  The driver entry
+// point is resolved once through the runtime (no -lcuda link dependency).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "sl_fast.cuh"
+
+namespace frg {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    if (!fn) throw Error(E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
+    FRG_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA field must be 16-byte aligned");
+    const cuuint64_t dims[2] = {(cuuint64_t)g.n2, (cuuint64_t)g.n0 * g.n1};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.n2 * 4};
+    const cuuint32_t box[2] = {TB_K, TB_J};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+}  // namespace frg

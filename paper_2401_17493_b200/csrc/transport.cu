@@ -9,7 +9,7 @@
 // Every SL time step is ONE launch of the shared-memory tiled gather engine
 // (sl_tile.cuh) with the step's pointwise update fused into its epilogue.
 #include "ops.h"
-#include "sl_tile.cuh"
+#include "sl_fast.cuh"
 
 namespace frg {
 
@@ -81,7 +81,7 @@ struct DepartureOp {
         d1 = dd[1];
         d2 = dd[2];
     }
-    __device__ __forceinline__ const VI* field(int f) const { return v[f]; }
+    __host__ __device__ __forceinline__ const VI* field(int f) const { return v[f]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
 #pragma unroll
         for (int c = 0; c < D; ++c) out[c][p] = (T(0.5) * sc[c]) * ((T)v[c][p] + vals[c]);
@@ -167,7 +167,7 @@ struct GatherOp {
     const T* in[NF];
     T* out[NF];
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int f) const { return in[f]; }
+    __host__ __device__ __forceinline__ const T* field(int f) const { return in[f]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[NF]) const {
 #pragma unroll
         for (int f = 0; f < NF; ++f) out[f][p] = vals[f];
@@ -230,9 +230,11 @@ struct AdjMultOp {
     T* cmul;
     T ht;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int) const { return divv; }
-    __device__ __forceinline__ void done(int p, const T (&vals)[1]) const {
-        T a = vals[0], b = divv[p];
+    __host__ __device__ __forceinline__ const T* field(int) const { return divv; }
+    using Pre = T;
+    __device__ __forceinline__ T pre(int p) const { return divv[p]; }
+    __device__ __forceinline__ void done(int p, const T (&vals)[1], T b) const {
+        T a = vals[0];
         cmul[p] = T(1) + T(0.5) * ht * (a + b + ht * a * b);
     }
 };
@@ -245,8 +247,10 @@ struct AdjStepOp {
     const T* cmul;
     T* out;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int) const { return u; }
-    __device__ __forceinline__ void done(int p, const T (&vals)[1]) const { out[p] = vals[0] * cmul[p]; }
+    __host__ __device__ __forceinline__ const T* field(int) const { return u; }
+    using Pre = T;
+    __device__ __forceinline__ T pre(int p) const { return cmul[p]; }
+    __device__ __forceinline__ void done(int p, const T (&vals)[1], T c) const { out[p] = vals[0] * c; }
 };
 
 template <typename T>

@@ -1,6 +1,6 @@
 // Deformation tensor (transport.py:197-221) and composed map (transport.py:224-247).
 #include "ops.h"
-#include "sl_tile.cuh"
+#include "sl_fast.cuh"
 
 namespace frg {
 
@@ -33,22 +33,16 @@ __device__ __forceinline__ void deform_update(int p, size_t N, T ht, const T* Fy
         }
 }
 
+// later steps: F holds F_j(y) (gathered in place), updated pointwise in place
 template <typename T, int D>
-struct DeformOp {
-    using V = T;
-    DispSrc<T> ds;
-    const T* Fin;
-    const T* jac_y;
-    const T* jac;
-    T* Fout;
-    size_t N;
-    T ht;
-    __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int f) const { return Fin + f * N; }
-    __device__ __forceinline__ void done(int p, const T (&vals)[D * D]) const {
-        deform_update<T, D>(p, N, ht, vals, jac_y, jac, Fout);
-    }
-};
+__global__ void k_deform_step(Dims g, T ht, const T* __restrict__ jac_y, const T* __restrict__ jac, T* F) {
+    Vox v;
+    if (!vox(g, v)) return;
+    T Fy[D * D];
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) Fy[e] = F[e * g.N + v.p];
+    deform_update<T, D>(v.p, g.N, ht, Fy, jac_y, jac, F);
+}
 
 // first step: F_y = I exactly (no gather)
 template <typename T, int D>
@@ -80,16 +74,18 @@ static void deformation_d(const Dims& g, int method, int n_t, const T* disp, con
     T ht = (T)(1.0 / n_t);
     k_deform_first<T, D><<<vox_grid(g), vox_block(), 0, st>>>(g, ht, jac_y, jac, bufs[0]);
     FRG_CHECK_LAUNCH();
+    // F_{s+1} = F_s(y) + Heun update: multi-field gather (3 fields per launch)
+    // into the output slot, then the 3x3 update in place
     for (int s = 1; s < n_t; ++s) {
-        DeformOp<T, D> op;
-        op.ds = disp_src(g, disp);
-        op.Fin = bufs[(s - 1) & 1];
-        op.jac_y = jac_y;
-        op.jac = jac;
-        op.Fout = bufs[s & 1];
-        op.N = g.N;
-        op.ht = ht;
-        launch_sl<T, D * D>(g, method, op, st);
+        const T* Fin = bufs[(s - 1) & 1];
+        T* Fout = bufs[s & 1];
+        for (size_t e = 0; e < dd; ++e) {
+            ins[e] = Fin + e * g.N;
+            outs[e] = Fout + e * g.N;
+        }
+        gather_fields(g, tcode(T(0)), method, disp, (int)dd, ins, outs, st);
+        k_deform_step<T, D><<<vox_grid(g), vox_block(), 0, st>>>(g, ht, jac_y, jac, Fout);
+        FRG_CHECK_LAUNCH();
     }
 }
 
@@ -123,7 +119,7 @@ struct ComposeOp {
     const T* Din[D];
     T* Dout[D];
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { cur.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int f) const { return step[f]; }
+    __host__ __device__ __forceinline__ const T* field(int f) const { return step[f]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
 #pragma unroll
         for (int c = 0; c < D; ++c) Dout[c][p] = Din[c][p] + vals[c];

@@ -1,6 +1,6 @@
 // Incremental state transport (transport.py:147-176): fused SL step kernels.
 #include "ops.h"
-#include "sl_tile.cuh"
+#include "sl_fast.cuh"
 
 #include <type_traits>
 
@@ -8,60 +8,65 @@ namespace frg {
 
 // ---------------------------------------------------------------------------
 // incremental state (transport.py:147-176)
-//   m~_{j+1} = m~_j(y) + h/2 (f0 + f1),  f0 = -grad m_j(y) . v~(y),
-//   f1 = -grad m_{j+1}(x) . v~(x);   m~_0 = 0.
-// grad m_j(y) is gathered once per velocity (grads_y); v~(y) once per call,
-// staged straight from the control-precision v~ (converted on the fly).
+//   m~_{j+1} = m~_j(y) + S_j,   S_j = h/2 (f0 + f1),
+//   f0 = -grad m_j(y) . v~(y),  f1 = -grad m_{j+1}(x) . v~(x);   m~_0 = 0.
+// S_j does not depend on m~, so ONE kernel gathers v~(y) (3 fields) and forms
+// every S_j from the per-velocity caches grad m_j(y) (grads_y) and grad m_j
+// (grads); m~_1 = S_0 exactly (m~_0(y) = 0).  Each later step is then a
+// single-field SL gather plus one add: m~_{j+1} = m~_j(y) + S_j.
 // ---------------------------------------------------------------------------
 template <typename T, int D>
 struct IncFirstOp {
     using V = T;
     DispSrc<T> ds;
     const T* vtT[D];
-    const T* gy0[D];
-    const T* gx1[D];
-    T* vty[D];
+    const T* gy;  // n_t x D x N, grad m_j at y
+    const T* gx;  // (n_t + 1) x D x N, grad m_j at x
+    size_t N;
+    int n_t;
     T* m1;
     T* fin;
-    T fsign, ht;
+    T* S;  // (n_t - 1) x N: S_1 .. S_{n_t-1}
+    T fsign, hh;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int f) const { return vtT[f]; }
+    __host__ __device__ __forceinline__ const T* field(int f) const { return vtT[f]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
-        T f0 = T(0), f1 = T(0);
+        T vx[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            vty[c][p] = vals[c];
-            f0 -= gy0[c][p] * vals[c];
-            f1 -= gx1[c][p] * vtT[c][p];
+        for (int c = 0; c < D; ++c) vx[c] = vtT[c][p];
+        for (int j = 0; j < n_t; ++j) {
+            T f0 = T(0), f1 = T(0);
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                f0 -= gy[((size_t)j * D + c) * N + p] * vals[c];
+                f1 -= gx[((size_t)(j + 1) * D + c) * N + p] * vx[c];
+            }
+            const T sj = hh * (f0 + f1);
+            if (j == 0) {
+                if (m1) m1[p] = sj;
+                if (fin) fin[p] = fsign * sj;
+            } else {
+                S[(size_t)(j - 1) * N + p] = sj;
+            }
         }
-        T m = T(0.5) * ht * (f0 + f1);
-        if (m1) m1[p] = m;
-        if (fin) fin[p] = fsign * m;
     }
 };
 
-template <typename T, int D>
+template <typename T>
 struct IncStepOp {
     using V = T;
     DispSrc<T> ds;
     const T* mj;
-    const T* vtT[D];
-    const T* vty[D];
-    const T* gyj[D];
-    const T* gx1[D];
+    const T* Sj;
     T* mnext;
     T* fin;
-    T fsign, ht;
+    T fsign;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
-    __device__ __forceinline__ const T* field(int) const { return mj; }
-    __device__ __forceinline__ void done(int p, const T (&vals)[1]) const {
-        T f0 = T(0), f1 = T(0);
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            f0 -= gyj[c][p] * vty[c][p];
-            f1 -= gx1[c][p] * vtT[c][p];
-        }
-        T m = vals[0] + T(0.5) * ht * (f0 + f1);
+    __host__ __device__ __forceinline__ const T* field(int) const { return mj; }
+    using Pre = T;
+    __device__ __forceinline__ T pre(int p) const { return Sj[p]; }
+    __device__ __forceinline__ void done(int p, const T (&vals)[1], T s) const {
+        const T m = vals[0] + s;
         if (mnext) mnext[p] = m;
         if (fin) fin[p] = fsign * m;
     }
@@ -69,14 +74,13 @@ struct IncStepOp {
 
 template <typename T, typename CV, int D>
 static void inc_state_d(const Dims& g, int method, int n_t, const T* disp, const T* grads, const T* grads_y,
-                        const CV* vt, T* vtT, T* vty, T* series, T* fin, T fsign, bool keep, cudaStream_t st) {
+                        const CV* vt, T* vtT, T* S, T* series, T* fin, T fsign, bool keep, cudaStream_t st) {
     const size_t N = g.N;
-    const size_t gs = (size_t)D * N;  // gradient slice stride
     T ht = (T)(1.0 / n_t);
     // slice buffers: keep == full series, else ping-pong in series[0..1]
     auto slice = [&](int j) -> T* { return keep ? series + (size_t)j * N : series + (size_t)(j & 1) * N; };
     if (keep) FRG_CUDA(cudaMemsetAsync(series, 0, sizeof(T) * N, st));
-    // v~ in transport precision once (the SL gathers stage it with cp.async)
+    // v~ in transport precision once (the SL gathers stage it from HBM)
     const T* vsrc;
     if constexpr (std::is_same<T, CV>::value) {
         vsrc = vt;
@@ -87,60 +91,54 @@ static void inc_state_d(const Dims& g, int method, int n_t, const T* disp, const
     {
         IncFirstOp<T, D> op;
         op.ds = disp_src(g, disp);
-        for (int c = 0; c < D; ++c) {
-            op.vtT[c] = vsrc + c * N;
-            op.gy0[c] = grads_y + c * N;
-            op.gx1[c] = grads + gs + c * N;
-            op.vty[c] = vty + c * N;
-        }
+        for (int c = 0; c < D; ++c) op.vtT[c] = vsrc + c * N;
+        op.gy = grads_y;
+        op.gx = grads;
+        op.N = N;
+        op.n_t = n_t;
         op.m1 = (n_t == 1 && !keep) ? nullptr : slice(1);
         op.fin = (n_t == 1) ? fin : nullptr;
+        op.S = S;
         op.fsign = fsign;
-        op.ht = ht;
+        op.hh = T(0.5) * ht;
         launch_sl<T, D>(g, method, op, st);
     }
     for (int j = 1; j < n_t; ++j) {
         bool last = (j == n_t - 1);
-        IncStepOp<T, D> op;
+        IncStepOp<T> op;
         op.ds = disp_src(g, disp);
         op.mj = slice(j);
-        for (int c = 0; c < D; ++c) {
-            op.vtT[c] = vsrc + c * N;
-            op.vty[c] = vty + c * N;
-            op.gyj[c] = grads_y + j * gs + c * N;
-            op.gx1[c] = grads + (j + 1) * gs + c * N;
-        }
+        op.Sj = S + (size_t)(j - 1) * N;
         op.mnext = (last && !keep) ? nullptr : slice(j + 1);
         op.fin = last ? fin : nullptr;
         op.fsign = fsign;
-        op.ht = ht;
         launch_sl<T, 1>(g, method, op, st);
     }
 }
 
 template <typename T, typename CV>
 static void inc_state_t(const Dims& g, int method, int n_t, const T* disp, const T* grads, const T* grads_y,
-                        const CV* vt, T* vtT, T* vty, T* series, T* fin, T fsign, bool keep, cudaStream_t st) {
+                        const CV* vt, T* vtT, T* S, T* series, T* fin, T fsign, bool keep, cudaStream_t st) {
     if (g.d == 3)
-        inc_state_d<T, CV, 3>(g, method, n_t, disp, grads, grads_y, vt, vtT, vty, series, fin, fsign, keep, st);
+        inc_state_d<T, CV, 3>(g, method, n_t, disp, grads, grads_y, vt, vtT, S, series, fin, fsign, keep, st);
     else
-        inc_state_d<T, CV, 2>(g, method, n_t, disp, grads, grads_y, vt, vtT, vty, series, fin, fsign, keep, st);
+        inc_state_d<T, CV, 2>(g, method, n_t, disp, grads, grads_y, vt, vtT, S, series, fin, fsign, keep, st);
 }
 
 void inc_state(const Dims& g, int tdtype, int cdtype, int method, int n_t, const void* disp, const void* grads,
-               const void* grads_y, const void* vt, void* vtT, void* vty, void* series, void* final_out,
+               const void* grads_y, const void* vt, void* vtT, void* S, void* series, void* final_out,
                double final_sign, bool keep_series, cudaStream_t st) {
     if (tdtype == F64 && cdtype == F64)
         inc_state_t<double, double>(g, method, n_t, (const double*)disp, (const double*)grads,
-                                    (const double*)grads_y, (const double*)vt, (double*)vtT, (double*)vty,
+                                    (const double*)grads_y, (const double*)vt, (double*)vtT, (double*)S,
                                     (double*)series, (double*)final_out, final_sign, keep_series, st);
     else if (tdtype == F32 && cdtype == F32)
         inc_state_t<float, float>(g, method, n_t, (const float*)disp, (const float*)grads, (const float*)grads_y,
-                                  (const float*)vt, (float*)vtT, (float*)vty, (float*)series, (float*)final_out,
+                                  (const float*)vt, (float*)vtT, (float*)S, (float*)series, (float*)final_out,
                                   (float)final_sign, keep_series, st);
     else if (tdtype == F32 && cdtype == F64)
         inc_state_t<float, double>(g, method, n_t, (const float*)disp, (const float*)grads, (const float*)grads_y,
-                                   (const double*)vt, (float*)vtT, (float*)vty, (float*)series, (float*)final_out,
+                                   (const double*)vt, (float*)vtT, (float*)S, (float*)series, (float*)final_out,
                                    (float)final_sign, keep_series, st);
     else
         throw Error(E_ARG, "inc_state: unsupported dtype combination");
