@@ -49,9 +49,16 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str | None 
     procs = []
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
               "-I", os.path.join(ROOT, "include"), *extra]
+    headers = [p for p in deps() if not p.endswith(".cu")]
+    newest_header = max(os.path.getmtime(p) for p in headers)
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
+        # incremental: an object is reused when it is newer than its source and
+        # every header (and the build flags did not change: variants use --force)
+        if (not force and out is None and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_header)):
+            continue
         cmd = common + ["-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = False

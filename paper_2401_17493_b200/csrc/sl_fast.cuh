@@ -185,6 +185,12 @@ struct SlfSmem {
     static constexpr size_t bytes = (size_t)NB * TB_VOL * sizeof(float) + 1024;
 };
 
+// Ops may take the whole per-thread tile in one epilogue call (done_tile)
+template <class Op, class = void>
+struct HasTile : std::false_type {};
+template <class Op>
+struct HasTile<Op, std::void_t<decltype(&Op::template done_tile<SL_TI>)>> : std::true_type {};
+
 template <class Op, class = void>
 struct PreOf {
     struct type {};
@@ -193,6 +199,69 @@ template <class Op>
 struct PreOf<Op, std::void_t<typename Op::Pre>> {
     using type = typename Op::Pre;
 };
+
+template <class Op, class = void>
+struct HasDs : std::false_type {};
+template <class Op>
+struct HasDs<Op, std::void_t<decltype(std::declval<const Op&>().ds.plan)>> : std::true_type {};
+
+__device__ __forceinline__ int4 encode_plan(int lo0, int lo1, int lo2, int S0, int S1, int S2) {
+    return make_int4(lo0, lo1, lo2, min(S0, 1023) | (min(S1, 1023) << 10) | (min(S2, 1023) << 20));
+}
+
+// One CTA per SL tile (same decomposition as k_slf): the stencil bounding box
+// of the tile's departure points -> plan[tile].
+template <typename T, int M>
+__global__ void __launch_bounds__(BX* BY) k_tile_plan(Dims g, DispSrc<T> ds, int4* __restrict__ plan) {
+    __shared__ int bb[6];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+    const int k = blockIdx.x * BX + tx, j = blockIdx.y * BY + ty, i_base = blockIdx.z * SL_TI;
+    if (tid < 6) bb[tid] = INT_MAX;
+    int mn0 = INT_MAX, mn1 = INT_MAX, mn2 = INT_MAX, mx0 = INT_MIN, mx1 = INT_MIN, mx2 = INT_MIN;
+    if (k < g.n2 && j < g.n1) {
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u) {
+            const int i = i_base + u;
+            if (i >= g.n0) continue;
+            T d0, d1, d2;
+            ds.get((i * g.n1 + j) * g.n2 + k, d0, d1, d2);
+            const int b0 = i + (int)Real<T>::floor_(d0), b1 = j + (int)Real<T>::floor_(d1),
+                      b2 = k + (int)Real<T>::floor_(d2);
+            mn0 = min(mn0, b0);
+            mx0 = max(mx0, b0);
+            mn1 = min(mn1, b1);
+            mx1 = max(mx1, b1);
+            mn2 = min(mn2, b2);
+            mx2 = max(mx2, b2);
+        }
+    }
+    mn0 = warp_min_i(mn0);
+    mn1 = warp_min_i(mn1);
+    mn2 = warp_min_i(mn2);
+    mx0 = warp_max_i(mx0);
+    mx1 = warp_max_i(mx1);
+    mx2 = warp_max_i(mx2);
+    __syncthreads();
+    if (tx == 0 && mn0 != INT_MAX) {
+        atomicMin(&bb[0], mn0);
+        atomicMin(&bb[1], mn1);
+        atomicMin(&bb[2], mn2);
+        atomicMin(&bb[3], -mx0);
+        atomicMin(&bb[4], -mx1);
+        atomicMin(&bb[5], -mx2);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int t = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        if (bb[0] == INT_MAX) {
+            plan[t] = make_int4(0, 0, 0, -1);
+        } else {
+            const int lo0 = bb[0] - Halo<M>::lo, lo1 = bb[1] - Halo<M>::lo, lo2 = (bb[2] - Halo<M>::lo) & ~3;
+            plan[t] = encode_plan(lo0, lo1, lo2, -bb[3] + Halo<M>::hi - lo0 + 1, -bb[4] + Halo<M>::hi - lo1 + 1,
+                                  -bb[5] + Halo<M>::hi - lo2 + 1);
+        }
+    }
+}
 
 // Lagrange weights for two points at once (Blackwell paired fp32: FADD2/FMUL2),
 // lane-for-lane identical to lagrange4f
@@ -246,7 +315,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 }
 
 template <int M, int NF, class Op>
-__global__ void __launch_bounds__(BX* BY, 4)
+__global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
     static_assert(M == LINEAR || M == CUBIC, "k_slf: linear / cubic only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
@@ -267,6 +336,26 @@ __global__ void __launch_bounds__(BX* BY, 4)
     }
     if (tid < 6) bb[tid] = INT_MAX;
 
+    const int4* plan = nullptr;
+    if constexpr (HasDs<Op>::value) plan = op.ds.plan;
+    int4 pe = make_int4(0, 0, 0, 0);
+    if (plan) pe = __ldg(plan + (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+
+    int lo0, lo1, lo2, S0, S1, S2;
+    if (plan) {
+        // precomputed box: issue the TMA first (the displacement loads below
+        // overlap its latency), no block reduction
+        if (pe.w < 0) return;  // empty tile
+        lo0 = pe.x;
+        lo1 = pe.y;
+        lo2 = pe.z;
+        S0 = pe.w & 1023;
+        S1 = (pe.w >> 10) & 1023;
+        S2 = (pe.w >> 20) & 1023;
+        if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
+            tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
+        __syncthreads();  // barrier initialised before anyone waits on it
+    }
     int base0[SL_TI], base1[SL_TI], base2[SL_TI];
     float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
     bool ok[SL_TI];
@@ -293,6 +382,7 @@ __global__ void __launch_bounds__(BX* BY, 4)
             mx2 = max(mx2, base2[u]);
         }
     }
+    if (!plan) {
     // CTA bounding box: warp REDUX, then 6 shared atomics per warp
     mn0 = warp_min_i(mn0);
     mn1 = warp_min_i(mn1);
@@ -317,12 +407,16 @@ __global__ void __launch_bounds__(BX* BY, 4)
     mx0 = -bb[3];
     mx1 = -bb[4];
     mx2 = -bb[5];
-    const int lo0 = mn0 - Halo<M>::lo, lo1 = mn1 - Halo<M>::lo, lo2 = (mn2 - Halo<M>::lo) & ~3;
-    const int S0 = mx0 + Halo<M>::hi - lo0 + 1;
-    const int S1 = mx1 + Halo<M>::hi - lo1 + 1;
-    const int S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    lo0 = mn0 - Halo<M>::lo;
+    lo1 = mn1 - Halo<M>::lo;
+    lo2 = (mn2 - Halo<M>::lo) & ~3;
+    S0 = mx0 + Halo<M>::hi - lo0 + 1;
+    S1 = mx1 + Halo<M>::hi - lo1 + 1;
+    S2 = mx2 + Halo<M>::hi - lo2 + 1;
+    if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
+        tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
+    }
     const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
-    if (fits && use_tma && tid == 0) tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
 
     // epilogue inputs: loads in flight while the box lands and the stencils run
     using PreT = typename PreOf<Op>::type;
@@ -394,6 +488,10 @@ __global__ void __launch_bounds__(BX* BY, 4)
                                    : 0.f;
         }
     }
+    if constexpr (HasTile<Op>::value) {
+        op.template done_tile<SL_TI>((i_base * g.n1 + j) * g.n2 + k, g.n1 * g.n2, ok, vals);
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < SL_TI; ++u)
         if (ok[u]) {
@@ -405,8 +503,19 @@ __global__ void __launch_bounds__(BX* BY, 4)
         }
 }
 
+// host: build the tile plan of an fp32 displacement map for `method`
+// (plan: sl_grid(g) tiles of int4)
+void build_tile_plan(const Dims& g, int method, const float* disp, int4* plan, cudaStream_t st);
+inline size_t tile_plan_count(const Dims& g) {
+    const dim3 gr = sl_grid(g);
+    return (size_t)gr.x * gr.y * gr.z;
+}
+
 template <int M, int NF, class Op>
-void launch_slf(const Dims& g, const Op& op, cudaStream_t st) {
+void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
+    Op op = op_in;
+    if constexpr (HasDs<Op>::value)
+        if (op.ds.plan && plan_method(op.ds.plan) != M) op.ds.plan = nullptr;
     TmaMaps<NF> maps;
     const int use_tma = tma_grid_ok(g) ? 1 : 0;
     for (int f = 0; f < NF; ++f) {

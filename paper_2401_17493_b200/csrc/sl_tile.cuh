@@ -423,9 +423,15 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) 
 // ---------------------------------------------------------------------------
 // displacement sources (per grid axis; axis 0 is absent in 2D)
 // ---------------------------------------------------------------------------
+// A displacement map may carry a TILE PLAN: per SL tile, the stencil bounding
+// box (lo0, lo1, lo2 aligned down to 4, S0 | S1 << 10 | S2 << 20; w = -1 for an
+// empty tile), computed once per map (k_tile_plan) and reused by every SL step
+// on that map, so the SL kernels issue their box TMA as soon as the plan entry
+// arrives instead of after a displacement load + block reduction.
 template <typename T>
 struct DispSrc {
     const T* a[3];
+    const int4* plan;
     __device__ __forceinline__ void get(int p, T& d0, T& d1, T& d2) const {
         d0 = a[0] ? a[0][p] : T(0);
         d1 = a[1][p];
@@ -433,11 +439,38 @@ struct DispSrc {
     }
 };
 
+// Host-side, thread-local binding of a displacement buffer to its plan for the
+// duration of a scope (the context binds disp_f / disp_b around its solves);
+// disp_src() attaches the plan when the map pointer and method match.
+struct PlanBinding {
+    const void* disp = nullptr;
+    const int4* plan = nullptr;
+    int method = -1;
+};
+inline thread_local PlanBinding g_plan_bind[2];
+struct PlanScope {
+    int slot;
+    PlanScope(int s, const void* disp, const int4* plan, int method) : slot(s) {
+        g_plan_bind[s].disp = disp;
+        g_plan_bind[s].plan = plan;
+        g_plan_bind[s].method = method;
+    }
+    ~PlanScope() { g_plan_bind[slot] = PlanBinding(); }
+};
+inline int plan_method(const int4* plan) {
+    for (const PlanBinding& b : g_plan_bind)
+        if (b.plan == plan) return b.method;
+    return -1;
+}
+
 template <typename T>
 inline DispSrc<T> disp_src(const Dims& g, const T* disp) {
     DispSrc<T> s;
     s.a[0] = s.a[1] = s.a[2] = nullptr;
+    s.plan = nullptr;
     for (int c = 0; c < g.d; ++c) s.a[g.comp_axis(c)] = disp + (size_t)c * g.N;
+    for (const PlanBinding& b : g_plan_bind)
+        if (b.disp == (const void*)disp && b.plan) s.plan = b.plan;
     return s;
 }
 

@@ -15,6 +15,8 @@
 #include "ops.h"
 #include "spectral.h"
 
+#include <type_traits>
+
 namespace frg {
 
 #define FRG_CUFFT(call)                                                                   \
@@ -245,37 +247,59 @@ __global__ void k_spec_scale(Dims g, long long nh, int ncomp, C* __restrict__ x,
 
 // out = alpha sym a + P(b), both normalised; written into a's spectrum.
 // a may be null (P(b) only, written into b's spectrum converted to A).
+// The per-bin arithmetic runs in the wider of the two spectra's precisions
+// (fp32 spectra: fp32 math, no fp64 divisions on the fp32 path).
 template <typename CA, typename CB>
 __global__ void k_spec_combine(Dims g, long long nh, CA* __restrict__ a, const CB* __restrict__ bsp, RegSpec r,
                                double invN, bool have_a, bool project) {
+    using RA = typename CR<CA>::R;
+    using RB = typename CR<CB>::R;
+    using M = typename std::conditional<(sizeof(RA) > sizeof(RB)), RA, RB>::type;
     int i0, i1, i2, p;
     if (!spec_vox(g, i0, i1, i2, p)) return;
-    Bin bn = bin_of(g, i0, i1, i2);
-    double ksq = bn.m[0] * bn.m[0] + bn.m[1] * bn.m[1] + bn.m[2] * bn.m[2];
-    double sa = have_a ? r.alpha * reg_sym(ksq, r) * invN : 0.0;
-    double br[3], bi[3], k[3] = {0, 0, 0}, mfac = 0.0;
+    const Bin bn = bin_of(g, i0, i1, i2);
+    M sa = M(0);
+    if (have_a) {
+        const M ksq = M(bn.m[0] * bn.m[0] + bn.m[1] * bn.m[1] + bn.m[2] * bn.m[2]);
+        M s = r.seminorm ? ksq : M(1) + ksq;
+        const M base = s;
+        for (int o = 1; o < r.order; ++o) s *= base;
+        sa = M(r.alpha) * s * M(invN);
+    }
+    M br[3], bi[3], k[3] = {M(0), M(0), M(0)}, mfac = M(0);
     for (int c = 0; c < g.d; ++c) {
         CB v = bsp[(long long)c * nh + p];
-        br[c] = v.x;
-        bi[c] = v.y;
+        br[c] = (M)v.x;
+        bi[c] = (M)v.y;
     }
-    if (project) proj_k(g, bn, r, k, mfac);
-    double dr = 0.0, di = 0.0;
+    if (project && r.incomp != 0) {
+        for (int q = 0; q < 3; ++q) k[q] = bn.nyq[q] ? M(0) : M(bn.m[q]);
+        const M ksq = k[0] * k[0] + k[1] * k[1] + k[2] * k[2];
+        if (ksq != M(0)) {
+            M mult = M(1);
+            if (r.incomp == 2) {
+                const M inner = M(r.beta) * (M(1) / ksq + M(1));
+                mult = M(1) / (M(r.alpha) / inner + M(1));
+            }
+            mfac = mult / ksq;
+        }
+    }
+    M dr = M(0), di = M(0);
     for (int c = 0; c < g.d; ++c) {
-        double kc = k[g.comp_axis(c)];
+        const M kc = k[g.comp_axis(c)];
         dr += kc * br[c];
         di += kc * bi[c];
     }
-    using RA = typename CR<CA>::R;
+    const M iN = M(invN);
     for (int c = 0; c < g.d; ++c) {
-        double kc = k[g.comp_axis(c)];
-        double orr = (br[c] - kc * mfac * dr) * invN;
-        double oi = (bi[c] - kc * mfac * di) * invN;
+        const M kc = k[g.comp_axis(c)];
+        M orr = (br[c] - kc * mfac * dr) * iN;
+        M oi = (bi[c] - kc * mfac * di) * iN;
         CA o;
         if (have_a) {
             CA av = a[(long long)c * nh + p];
-            orr += sa * av.x;
-            oi += sa * av.y;
+            orr += sa * (M)av.x;
+            oi += sa * (M)av.y;
         }
         o.x = (RA)orr;
         o.y = (RA)oi;

@@ -35,4 +35,16 @@ void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
     if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+void build_tile_plan(const Dims& g, int method, const float* disp, int4* plan, cudaStream_t st) {
+    DispSrc<float> ds = disp_src(g, disp);
+    ds.plan = nullptr;
+    if (method == CUBIC)
+        k_tile_plan<float, CUBIC><<<sl_grid(g), vox_block(), 0, st>>>(g, ds, plan);
+    else if (method == LINEAR)
+        k_tile_plan<float, LINEAR><<<sl_grid(g), vox_block(), 0, st>>>(g, ds, plan);
+    else
+        throw Error(E_ARG, "tile plans are built for linear / cubic maps");
+    FRG_CHECK_LAUNCH();
+}
+
 }  // namespace frg

@@ -30,6 +30,46 @@ struct IncFirstOp {
     T fsign, hh;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int f) const { return vtT[f]; }
+    // Tile epilogue (the TI voxels of one thread, p0 + u * pstride): the
+    // gradient loads of all voxels for one j are independent read-only loads
+    // in flight together, instead of one dependent round trip per voxel and j.
+    template <int TI>
+    __device__ __forceinline__ void done_tile(int p0, int pstride, const bool (&ok)[TI],
+                                              const T (&vals)[TI][D]) const {
+        T vx[TI][D];
+#pragma unroll
+        for (int u = 0; u < TI; ++u)
+#pragma unroll
+            for (int c = 0; c < D; ++c) vx[u][c] = ok[u] ? __ldg(vtT[c] + p0 + u * pstride) : T(0);
+        for (int j = 0; j < n_t; ++j) {
+            const T* __restrict__ gyj = gy + (size_t)j * D * N + p0;
+            const T* __restrict__ gxj = gx + (size_t)(j + 1) * D * N + p0;
+            T sj[TI];
+#pragma unroll
+            for (int u = 0; u < TI; ++u) {
+                T f0 = T(0), f1 = T(0);
+                if (ok[u]) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        f0 -= __ldg(gyj + c * N + u * pstride) * vals[u][c];
+                        f1 -= __ldg(gxj + c * N + u * pstride) * vx[u][c];
+                    }
+                }
+                sj[u] = hh * (f0 + f1);
+            }
+#pragma unroll
+            for (int u = 0; u < TI; ++u) {
+                if (!ok[u]) continue;
+                const int p = p0 + u * pstride;
+                if (j == 0) {
+                    if (m1) m1[p] = sj[u];
+                    if (fin) fin[p] = fsign * sj[u];
+                } else {
+                    S[(size_t)(j - 1) * N + p] = sj[u];
+                }
+            }
+        }
+    }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
         T vx[D];
 #pragma unroll
