@@ -180,6 +180,54 @@ int frg_kkt_get(frg_kkt* k, int32_t which, void* dst);
 /* determinant stats of F(1) for the current velocity {min, mean, max}   optimizer.py:169-171 */
 int frg_kkt_detgrad(frg_kkt* k, double out[3]);
 
+/* ---------------------------------------------------------------------------
+ * Slab decomposition (multi-GPU; the reference has none — CLAIRE's MPI slab
+ * decomposition is described in PAPER.md:500-545 and SURVEY.md §8e).  Rank r
+ * owns n_loc[0] consecutive planes of a 3D grid with n0_glob planes along
+ * axis 0.  Arrays named *_src carry h0 ghost planes before and after the
+ * owned planes per component ((n_loc[0] + 2 h0) planes, filled by the caller's
+ * halo exchange); all other arrays are (n_loc[0], n1, n2).  fp32 transport,
+ * linear or cubic.  The host (dist.py) exchanges ghost planes and runs the
+ * all-to-all transposes between these calls.
+ * ------------------------------------------------------------------------- */
+int frg_slab_departure(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, double h_t,
+                       const void* v_src, const void* v_loc, void* disp, void* stream);
+int frg_slab_gather(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
+                    int32_t nf, const void* const* in_src, void* const* out, void* stream);
+int frg_slab_adjoint_multiplier(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, double h_t,
+                                const void* disp_b, const void* divv_src, const void* divv_loc, void* cmul,
+                                void* stream);
+int frg_slab_adjoint_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp_b,
+                          const void* cmul, const void* u_src, void* out, void* stream);
+/* first incremental-state step: gathers v~ (vt_src), writes m~_1 and the Heun
+ * sources S_1..S_{n_t-1} ((n_t-1) x N) from grad m_j (grads, (n_t+1) x 3 x N)
+ * and grad m_j(y) (grads_y, n_t x 3 x N) */
+int frg_slab_inc_first(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, int32_t n_t,
+                       const void* disp, const void* grads, const void* grads_y, const void* vt_src,
+                       const void* vt_loc, void* m1, void* S, void* stream);
+int frg_slab_inc_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
+                      const void* m_src, const void* S_j, void* m_next, void* stream);
+int frg_slab_fd8_gradient(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t nslices, const void* u_src,
+                          void* out, void* stream);
+int frg_slab_fd8_divergence(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, const void* v_src, void* out,
+                            void* stream);
+/* batched 2D R2C (dir = 1) / C2R (dir = -1, unnormalised) over axes (1, 2) of
+ * the owned planes: real (ncomp, n0_loc, n1, n2) <-> complex (ncomp, n0_loc, n1, n2/2+1) */
+int frg_slab_fft2(const int32_t n_loc[3], int32_t dtype, int32_t ncomp, int32_t dir, const void* in, void* out,
+                  void* stream);
+/* in-place 1D C2C along axis 0 of the axis-1 split spectrum (ncomp, n0_glob, n1_loc, n2/2+1) */
+int frg_slab_fft1(int32_t n0_glob, int32_t n1_loc, int32_t n2, int32_t dtype, int32_t ncomp, int32_t dir, void* data,
+                  void* stream);
+/* dir = 1: (n0_loc, n1, nh) -> (nranks, n0_loc, n1/nranks, nh) per component; dir = -1: inverse */
+int frg_slab_transpose(int32_t dir, int32_t nranks, const int32_t n_loc[3], int32_t dtype, int32_t ncomp,
+                       const void* src, void* dst, void* stream);
+/* symbol (FRG_SYM_*) / N on the split spectrum of rows [i1_off, i1_off + n1_loc) */
+int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, int32_t ncomp,
+                        void* x, int32_t kind, const frg_reg* reg, void* stream);
+/* a = alpha L a + P(b) (normalised); a == b: P(b) only */
+int frg_slab_spec_combine(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, void* a,
+                          const void* b, const frg_reg* reg, int32_t project, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

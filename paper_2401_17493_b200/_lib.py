@@ -93,6 +93,20 @@ PROTOTYPES = {
     "frg_kkt_set_counters": [_P, ctypes.POINTER(_L)],
     "frg_kkt_get": [_P, _I, _P],
     "frg_kkt_detgrad": [_P, _DP],
+    # slab decomposition (multi-GPU, dist.py)
+    "frg_slab_departure": [_N3, _I, _I, _I, _D, _P, _P, _P, _P],
+    "frg_slab_gather": [_N3, _I, _I, _I, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _P],
+    "frg_slab_adjoint_multiplier": [_N3, _I, _I, _I, _D, _P, _P, _P, _P, _P],
+    "frg_slab_adjoint_step": [_N3, _I, _I, _I, _P, _P, _P, _P, _P],
+    "frg_slab_inc_first": [_N3, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "frg_slab_inc_step": [_N3, _I, _I, _I, _P, _P, _P, _P, _P],
+    "frg_slab_fd8_gradient": [_N3, _I, _I, _I, _P, _P, _P],
+    "frg_slab_fd8_divergence": [_N3, _I, _I, _P, _P, _P],
+    "frg_slab_fft2": [_N3, _I, _I, _I, _P, _P, _P],
+    "frg_slab_fft1": [_I, _I, _I, _I, _I, _I, _P, _P],
+    "frg_slab_transpose": [_I, _I, _N3, _I, _I, _P, _P, _P],
+    "frg_slab_spec_apply": [_N3, _I, _I, _I, _I, _P, _I, ctypes.POINTER(FrgReg), _P],
+    "frg_slab_spec_combine": [_N3, _I, _I, _I, _P, _P, ctypes.POINTER(FrgReg), _I, _P],
 }
 
 _lib = None

@@ -451,3 +451,137 @@ int frg_kkt_detgrad(frg_kkt* k, double out[3]) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// slab decomposition (multi-GPU; dist.py drives these per rank, exchanges in
+// between over torch.distributed / NCCL).  n_loc = {n0_loc, n1, n2} owned
+// planes of a 3D grid with n0_glob planes; *_src arrays carry h0 ghost planes
+// per component ((n0_loc + 2 h0) planes); fp32 transport.
+// ---------------------------------------------------------------------------
+static Dims slab_dims(const int32_t n_loc[3], int32_t n0_glob, int32_t h0) {
+    FRG_REQUIRE(n_loc != nullptr && n_loc[0] >= 1 && n_loc[1] >= 1 && n_loc[2] >= 1, "bad slab grid");
+    FRG_REQUIRE(n0_glob >= n_loc[0] && h0 >= 0, "bad slab decomposition");
+    Dims g = make_dims(n_loc, 3);
+    g.h0 = h0;
+    g.n0g = n0_glob;
+    return g;
+}
+static void check_slab_method(int m) { FRG_REQUIRE(m == 1 || m == 2, "slab transport: linear or cubic"); }
+
+extern "C" {
+
+int frg_slab_departure(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, double h_t,
+                       const void* v_src, const void* v_loc, void* disp, void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        departure(slab_dims(n_loc, n0_glob, h0), F32, F32, method, h_t, v_src, disp, ST(stream), v_loc);
+    });
+}
+
+int frg_slab_gather(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
+                    int32_t nf, const void* const* in_src, void* const* out, void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        FRG_REQUIRE(nf >= 1, "nf must be >= 1");
+        gather_fields(slab_dims(n_loc, n0_glob, h0), F32, method, disp, nf, in_src, out, ST(stream));
+    });
+}
+
+int frg_slab_adjoint_multiplier(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, double h_t,
+                                const void* disp_b, const void* divv_src, const void* divv_loc, void* cmul,
+                                void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        adjoint_multiplier(slab_dims(n_loc, n0_glob, h0), F32, method, h_t, disp_b, divv_src, cmul, ST(stream),
+                           divv_loc);
+    });
+}
+
+int frg_slab_adjoint_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp_b,
+                          const void* cmul, const void* u_src, void* out, void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        adjoint_step(slab_dims(n_loc, n0_glob, h0), F32, method, disp_b, cmul, u_src, out, ST(stream));
+    });
+}
+
+int frg_slab_inc_first(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, int32_t n_t,
+                       const void* disp, const void* grads, const void* grads_y, const void* vt_src,
+                       const void* vt_loc, void* m1, void* S, void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        FRG_REQUIRE(n_t >= 1, "n_t must be >= 1");
+        inc_first(slab_dims(n_loc, n0_glob, h0), method, n_t, (const float*)disp, (const float*)grads,
+                  (const float*)grads_y, (const float*)vt_src, (const float*)vt_loc, (float*)m1, (float*)S,
+                  ST(stream));
+    });
+}
+
+int frg_slab_inc_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
+                      const void* m_src, const void* S_j, void* m_next, void* stream) {
+    return guard([&] {
+        check_slab_method(method);
+        inc_step(slab_dims(n_loc, n0_glob, h0), method, (const float*)disp, (const float*)m_src, (const float*)S_j,
+                 (float*)m_next, ST(stream));
+    });
+}
+
+int frg_slab_fd8_gradient(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t nslices, const void* u_src,
+                          void* out, void* stream) {
+    return guard([&] {
+        FRG_REQUIRE(nslices >= 1, "nslices must be >= 1");
+        fd8_gradient(slab_dims(n_loc, n0_glob, h0), F32, nslices, u_src, out, ST(stream));
+    });
+}
+
+int frg_slab_fd8_divergence(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, const void* v_src, void* out,
+                            void* stream) {
+    return guard([&] { fd8_divergence(slab_dims(n_loc, n0_glob, h0), F32, v_src, out, ST(stream)); });
+}
+
+int frg_slab_fft2(const int32_t n_loc[3], int32_t dtype, int32_t ncomp, int32_t dir, const void* in, void* out,
+                  void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        FRG_REQUIRE(ncomp >= 1 && (dir == 1 || dir == -1), "bad slab fft2 arguments");
+        slab_fft2(n_loc[0], n_loc[1], n_loc[2], dtype, ncomp, dir, in, out, ST(stream));
+    });
+}
+
+int frg_slab_fft1(int32_t n0_glob, int32_t n1_loc, int32_t n2, int32_t dtype, int32_t ncomp, int32_t dir, void* data,
+                  void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        FRG_REQUIRE(ncomp >= 1 && (dir == 1 || dir == -1), "bad slab fft1 arguments");
+        slab_fft1(n0_glob, n1_loc * (n2 / 2 + 1), dtype, ncomp, dir, data, ST(stream));
+    });
+}
+
+int frg_slab_transpose(int32_t dir, int32_t nranks, const int32_t n_loc[3], int32_t dtype, int32_t ncomp,
+                       const void* src, void* dst, void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        slab_transpose(dir, nranks, n_loc[0], n_loc[1], n_loc[2] / 2 + 1, dtype == FRG_F64 ? 16 : 8, ncomp, src, dst,
+                       ST(stream));
+    });
+}
+
+int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, int32_t ncomp,
+                        void* x, int32_t kind, const frg_reg* reg, void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        FRG_REQUIRE(kind >= 0 && kind <= 6, "unknown symbol kind");
+        slab_spec_scale(dims_of(n_glob, 3), i1_off, n1_loc, dtype, ncomp, x, kind, reg_of(reg), ST(stream));
+    });
+}
+
+int frg_slab_spec_combine(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, void* a,
+                          const void* b, const frg_reg* reg, int32_t project, void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        slab_spec_combine(dims_of(n_glob, 3), i1_off, n1_loc, dtype, a, b, reg_of(reg), project != 0, ST(stream));
+    });
+}
+
+}  // extern "C"
+

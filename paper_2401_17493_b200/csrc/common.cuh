@@ -17,11 +17,22 @@
 
 namespace frg {
 
+// Slab decomposition (multi-GPU, dist.py): a rank owns n0 consecutive planes
+// of a global grid with n0g planes along axis 0.  SOURCE fields of the SL
+// gathers and FD8 stencils are then stored with h0 ghost planes before and
+// after the owned planes ((n0 + 2 h0, n1, n2), pointer at the first ghost
+// plane) and are not wrapped along axis 0; outputs, displacements and
+// epilogue inputs stay (n0, n1, n2).  h0 == 0 / n0g == 0: the periodic
+// single-GPU grid.
 struct Dims {
     int n0, n1, n2;  // n0 == 1 for 2D grids
     long long N;     // n0 * n1 * n2
     int d;           // vector components (2 or 3)
+    int h0 = 0;      // ghost planes of source fields along axis 0 (slab mode)
+    int n0g = 0;     // global axis-0 length (slab mode), 0 = n0
     __host__ __device__ int axis_len(int a) const { return a == 0 ? n0 : (a == 1 ? n1 : n2); }
+    // length of the full (global) axis: sets the grid spacing 2 pi / n
+    __host__ __device__ int axis_glob(int a) const { return (a == 0 && n0g > 0) ? n0g : axis_len(a); }
     __host__ __device__ int comp_axis(int c) const { return (3 - d) + c; }
 };
 
@@ -32,7 +43,17 @@ inline Dims make_dims(const int32_t n[3], int d) {
     g.n2 = n[2];
     g.N = (long long)g.n0 * g.n1 * g.n2;
     g.d = d;
+    g.h0 = 0;
+    g.n0g = 0;
     return g;
+}
+
+// source plane of (unwrapped) plane index b along axis 0
+__host__ __device__ __forceinline__ int src_plane(const Dims& g, int b) {
+    if (g.h0 > 0) return b + g.h0;
+    if ((unsigned)b < (unsigned)g.n0) return b;
+    int r = b % g.n0;
+    return r < 0 ? r + g.n0 : r;
 }
 
 enum Method { NEAREST = 0, LINEAR = 1, CUBIC = 2 };

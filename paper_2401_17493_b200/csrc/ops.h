@@ -14,8 +14,10 @@ void sample_q(const void* vals, int dtype, const Dims& g, const double* q0, cons
               const double* q2, long long npts, int method, void* out, cudaStream_t st);
 
 // RK2 departure displacement (index units) from velocity v (vdtype), d comps
+// (slab mode: v carries g.h0 ghost planes per component, vloc is v on the
+// owned planes; vloc == nullptr: v itself)
 void departure(const Dims& g, int tdtype, int vdtype, int method, double h_t, const void* v,
-               void* disp, cudaStream_t st);
+               void* disp, cudaStream_t st, const void* vloc = nullptr);
 // physical departure points y = x - h*disp (tdtype) and the inverse map
 void disp_to_points(const Dims& g, int tdtype, const void* disp, void* y, cudaStream_t st);
 void points_to_disp(const Dims& g, int tdtype, const void* y, void* disp, cudaStream_t st);
@@ -28,7 +30,13 @@ void solve_state(const Dims& g, int tdtype, int method, int n_t, const void* dis
                  cudaStream_t st);
 // adjoint multiplier c = 1 + h/2 (div(y_b) + div + h div(y_b) div)
 void adjoint_multiplier(const Dims& g, int tdtype, int method, double h_t, const void* disp_b,
-                        const void* divv, void* cmul, cudaStream_t st);
+                        const void* divv, void* cmul, cudaStream_t st, const void* divl = nullptr);
+// slab-mode incremental state pieces (fp32; sources with g.h0 ghost planes):
+// first step (gathers v~, forms S_0..S_{n_t-1}; m1 = S_0) and one later step
+void inc_first(const Dims& g, int method, int n_t, const float* disp, const float* grads, const float* grads_y,
+               const float* vt_src, const float* vt_loc, float* m1, float* S, cudaStream_t st);
+void inc_step(const Dims& g, int method, const float* disp, const float* m_src, const float* Sj, float* m_next,
+              cudaStream_t st);
 // one backward step: out = u(y_b) * c
 void adjoint_step(const Dims& g, int tdtype, int method, const void* disp_b, const void* cmul,
                   const void* u, void* out, cudaStream_t st);
@@ -120,5 +128,21 @@ double reg_energy(const Dims& g, int dtype, const void* v, const RegSpec& r, cud
 void restrict_field(const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
 void prolong_field(const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
 void spectral_release_plans();
+
+// ---- slab-decomposed spectral pieces (spectral.cu; multi-GPU, dist.py) ------
+// batched 2D R2C (dir > 0) / C2R (dir < 0, unnormalised) over axes (1, 2) of
+// n0_loc planes x ncomp: real (ncomp, n0_loc, n1, n2) <-> complex (ncomp, n0_loc, n1, nh)
+void slab_fft2(int n0_loc, int n1, int n2, int dtype, int ncomp, int dir, const void* in, void* out, cudaStream_t st);
+// in-place batched 1D C2C along axis 0 of (ncomp, n0, cols) complex (cols = n1_loc * nh)
+void slab_fft1(int n0, int cols, int dtype, int ncomp, int dir, void* data, cudaStream_t st);
+// (n0_loc, n1, nh) <-> (P, n0_loc, n1/P, nh) per component (all-to-all staging)
+void slab_transpose(int dir, int P, int n0_loc, int n1, int nh, int elem_bytes, int ncomp, const void* src, void* dst,
+                    cudaStream_t st);
+// on the axis-1 split spectrum (ncomp, n0, n1_loc, nh) of the GLOBAL grid g
+void slab_spec_scale(const Dims& g, int i1_off, int n1_loc, int dtype, int ncomp, void* x, int kind,
+                     const RegSpec& r, cudaStream_t st);
+// a = alpha L a + P(b) (normalised); a == b: P(b) only
+void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a, const void* b, const RegSpec& r,
+                       bool project, cudaStream_t st);
 
 }  // namespace frg

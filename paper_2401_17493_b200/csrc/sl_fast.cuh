@@ -50,7 +50,9 @@ struct alignas(64) TmaMaps {
 // (n0*n1, n2), box TB_J rows x TB_K columns
 void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g);
 // host: whether the TMA engine applies to this grid (every axis >= its box edge)
-inline bool tma_grid_ok(const Dims& g) { return g.n0 >= TB_I && g.n1 >= TB_J && g.n2 >= TB_K && (g.n2 % 4) == 0; }
+inline bool tma_grid_ok(const Dims& g) {
+    return (g.h0 > 0 || g.n0 >= TB_I) && g.n1 >= TB_J && g.n2 >= TB_K && (g.n2 % 4) == 0;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -83,7 +85,7 @@ __device__ __forceinline__ void tma_load_2d(float* dst, const CUtensorMap* map, 
 __device__ __forceinline__ void tma_box(float* box, const CUtensorMap* map, const Dims& g, int lo0, int lo1, int lo2,
                                         int S0, uint64_t* bar) {
     mbar_expect_tx(bar, (unsigned)(S0 * TB_PLANE * sizeof(float)));
-    for (int a = 0; a < S0; ++a) tma_load_2d(box + a * TB_PLANE, map, lo2, wrap_near(lo0 + a, g.n0) * g.n1 + lo1, bar);
+    for (int a = 0; a < S0; ++a) tma_load_2d(box + a * TB_PLANE, map, lo2, src_plane(g, lo0 + a) * g.n1 + lo1, bar);
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
@@ -158,7 +160,7 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
         } else {
             a = in1; b = in2; c = x;
         }
-        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
         cp_async_elem<4>(box + (a * TB_J + b) * TB_K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
     }
 }
@@ -172,7 +174,7 @@ __device__ __forceinline__ void stage_fixed(float* __restrict__ box, const float
         const int c = e - r * S2;
         const int a = r / S1;
         const int b = r - a * S1;
-        const int gi = wrap_near(lo0 + a, g.n0), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
         cp_async_elem<4>(box + (a * TB_J + b) * TB_K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
     }
 }
@@ -429,7 +431,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
 
     float vals[SL_TI][NF];
     if (fits) {
-        const bool wrap = lo0 < 0 || lo0 + S0 > g.n0 || lo1 < 0 || lo1 + S1 > g.n1 || lo2 < 0 || lo2 + S2 > g.n2;
+        // (planes never need a patch: tma_box / stage_fixed resolve them)
+        const bool wrap = lo1 < 0 || lo1 + S1 > g.n1 || lo2 < 0 || lo2 + S2 > g.n2;
         // per-voxel smem offset of the first tap (same for every field)
         int off[SL_TI];
 #pragma unroll
@@ -478,13 +481,16 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
             }
         }
     } else {
+        // source-grid view: ghost planes are ordinary planes of a taller grid
+        Dims gsrc = g;
+        gsrc.n0 = g.n0 + 2 * g.h0;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const float* src = op.field(f);
 #pragma unroll
             for (int u = 0; u < SL_TI; ++u)
-                vals[u][f] = ok[u] ? global_interp<float, M, float>(g, src, base0[u], base1[u], base2[u], fr0[u],
-                                                                    fr1[u], fr2[u])
+                vals[u][f] = ok[u] ? global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u], base2[u],
+                                                                    fr0[u], fr1[u], fr2[u])
                                    : 0.f;
         }
     }

@@ -484,6 +484,7 @@ inline dim3 sl_grid(const Dims& g) {
 
 template <typename T, int NF, class Op>
 void launch_sl_generic(const Dims& g, int method, const Op& op, cudaStream_t st) {
+    FRG_REQUIRE(g.h0 == 0, "slab (ghost-plane) SL steps need fp32 linear / cubic transport");
     switch (method) {
         case NEAREST: k_sl<T, NEAREST, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
         case LINEAR: k_sl<T, LINEAR, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;

@@ -662,3 +662,232 @@ void prolong_field(const Dims& gf, int dtype, const void* in, void* out, cudaStr
 }
 
 }  // namespace frg
+
+namespace frg {
+
+// ===========================================================================
+// Slab-decomposed spectral operators (multi-GPU, dist.py).
+//
+// Rank r owns planes [r n0/P, (r+1) n0/P) of the real field.  Forward:
+//   (1) batched 2D R2C over axes (1, 2) of every owned plane  -> (n0/P, n1, nh)
+//   (2) pack to (P, n0/P, n1/P, nh) and all-to-all (host, NCCL)  -> (n0, n1/P, nh)
+//   (3) batched 1D C2C along axis 0 (stride n1/P * nh)
+// The pointwise operators then act on the axis-1 split spectrum with global
+// frequencies (i1 = r n1/P + local row); the inverse runs the steps backwards.
+// ===========================================================================
+namespace {
+std::map<std::tuple<int, int, int, int>, cufftHandle> g_slab1d;
+std::mutex g_slab1d_mu;
+}  // namespace
+
+template <typename R>
+void slab_fft2_t(int n0_loc, int n1, int n2, int ncomp, int dir, const void* in, void* out, cudaStream_t st) {
+    Dims p;  // one plane: rank-2 (n1, n2) plans from the shared cache, batched over planes x comps
+    p.n0 = 1;
+    p.n1 = n1;
+    p.n2 = n2;
+    p.N = (long long)n1 * n2;
+    p.d = 3;
+    if (dir > 0)
+        fwd<R>(g_plans, p, n0_loc * ncomp, (const R*)in, (typename CT<R>::C*)out, st);
+    else
+        inv<R>(g_plans, p, n0_loc * ncomp, (typename CT<R>::C*)in, (R*)out, st);
+}
+
+void slab_fft2(int n0_loc, int n1, int n2, int dtype, int ncomp, int dir, const void* in, void* out, cudaStream_t st) {
+    if (dtype == F64)
+        slab_fft2_t<double>(n0_loc, n1, n2, ncomp, dir, in, out, st);
+    else
+        slab_fft2_t<float>(n0_loc, n1, n2, ncomp, dir, in, out, st);
+}
+
+void slab_fft1(int n0, int cols, int dtype, int ncomp, int dir, void* data, cudaStream_t st) {
+    const int type = dtype == F64 ? CUFFT_Z2Z : CUFFT_C2C;
+    cufftHandle h;
+    {
+        std::lock_guard<std::mutex> lk(g_slab1d_mu);
+        auto key = std::make_tuple(n0, cols, type, 0);
+        auto it = g_slab1d.find(key);
+        if (it == g_slab1d.end()) {
+            int n[1] = {n0};
+            FRG_CUFFT(cufftPlanMany(&h, 1, n, n, cols, 1, n, cols, 1, (cufftType)type, cols));
+            g_slab1d[key] = h;
+        } else {
+            h = it->second;
+        }
+    }
+    FRG_CUFFT(cufftSetStream(h, st));
+    const size_t es = dtype == F64 ? 16 : 8;
+    for (int c = 0; c < ncomp; ++c) {
+        char* x = (char*)data + (size_t)c * n0 * cols * es;
+        if (dtype == F64)
+            FRG_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)x, (cufftDoubleComplex*)x,
+                                   dir > 0 ? CUFFT_FORWARD : CUFFT_INVERSE));
+        else
+            FRG_CUFFT(cufftExecC2C(h, (cufftComplex*)x, (cufftComplex*)x, dir > 0 ? CUFFT_FORWARD : CUFFT_INVERSE));
+    }
+}
+
+// pack (dir > 0): (n0_loc, n1, nh) -> (P, n0_loc, n1/P, nh);  unpack (dir < 0): inverse.
+// One thread per element, 8- or 16-byte complex elements, per component.
+template <typename E>
+__global__ void k_slab_transpose(int dir, int P, int n0_loc, int n1, int nh, int ncomp, const E* __restrict__ src,
+                                 E* __restrict__ dst) {
+    const long long per = (long long)n0_loc * n1 * nh;
+    const long long total = per * ncomp;
+    const int n1l = n1 / P;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long c = e / per;
+        long long r = e - c * per;
+        // natural index (i0, i1, i2) of the (n0_loc, n1, nh) layout
+        const int i2 = (int)(r % nh);
+        r /= nh;
+        const int i1 = (int)(r % n1);
+        const int i0 = (int)(r / n1);
+        const int q = i1 / n1l, a = i1 - q * n1l;
+        const long long packed = c * per + (((long long)q * n0_loc + i0) * n1l + a) * nh + i2;
+        const long long natural = e;
+        if (dir > 0)
+            dst[packed] = src[natural];
+        else
+            dst[natural] = src[packed];
+    }
+}
+
+void slab_transpose(int dir, int P, int n0_loc, int n1, int nh, int elem_bytes, int ncomp, const void* src, void* dst,
+                    cudaStream_t st) {
+    FRG_REQUIRE(P >= 1 && n1 % P == 0, "slab transpose: n1 must be divisible by the rank count");
+    const long long total = (long long)n0_loc * n1 * nh * ncomp;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    if (elem_bytes == 16)
+        k_slab_transpose<double2><<<blocks, 256, 0, st>>>(dir, P, n0_loc, n1, nh, ncomp, (const double2*)src,
+                                                           (double2*)dst);
+    else
+        k_slab_transpose<float2><<<blocks, 256, 0, st>>>(dir, P, n0_loc, n1, nh, ncomp, (const float2*)src,
+                                                          (float2*)dst);
+    FRG_CHECK_LAUNCH();
+}
+
+// element (i0, a, i2) of the axis-1 split spectrum (n0, n1_loc, nh) -> global bin
+__device__ __forceinline__ bool slab_spec_vox(const Dims& g, int i1_off, int n1_loc, long long e, int& i0, int& i1,
+                                              int& i2) {
+    const int nh = g.n2 / 2 + 1;
+    i2 = (int)(e % nh);
+    const long long r = e / nh;
+    const int a = (int)(r % n1_loc);
+    i0 = (int)(r / n1_loc);
+    i1 = i1_off + a;
+    return i0 < g.n0;
+}
+
+// x *= symbol(kind) / N for ncomp spectra (same symbols as k_spec_scale)
+template <typename C>
+__global__ void k_slab_spec_scale(Dims g, int i1_off, int n1_loc, int ncomp, C* __restrict__ x, int kind, RegSpec r,
+                                  double invN) {
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+         e += (long long)gridDim.x * blockDim.x) {
+        int i0, i1, i2;
+        slab_spec_vox(g, i1_off, n1_loc, e, i0, i1, i2);
+        const double s = symbol_of(g, bin_of(g, i0, i1, i2), kind, r) * invN;
+        using R = typename CR<C>::R;
+        for (int c = 0; c < ncomp; ++c) {
+            C v = x[(long long)c * cnt + e];
+            v.x = (R)(v.x * s);
+            v.y = (R)(v.y * s);
+            x[(long long)c * cnt + e] = v;
+        }
+    }
+}
+
+// a = alpha sym a + P(b), both normalised (k_spec_combine on the split spectrum)
+template <typename C>
+__global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, C* __restrict__ a, const C* __restrict__ bsp,
+                               RegSpec r, double invN, bool have_a, bool project) {
+    using M = typename CR<C>::R;
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+         e += (long long)gridDim.x * blockDim.x) {
+        int i0, i1, i2;
+        slab_spec_vox(g, i1_off, n1_loc, e, i0, i1, i2);
+        const Bin bn = bin_of(g, i0, i1, i2);
+        M sa = M(0);
+        if (have_a) {
+            const M ksq = M(bn.m[0] * bn.m[0] + bn.m[1] * bn.m[1] + bn.m[2] * bn.m[2]);
+            M s = r.seminorm ? ksq : M(1) + ksq;
+            const M base = s;
+            for (int o = 1; o < r.order; ++o) s *= base;
+            sa = M(r.alpha) * s * M(invN);
+        }
+        M br[3], bi[3], k[3] = {M(0), M(0), M(0)}, mfac = M(0);
+        for (int c = 0; c < g.d; ++c) {
+            C v = bsp[(long long)c * cnt + e];
+            br[c] = v.x;
+            bi[c] = v.y;
+        }
+        if (project && r.incomp != 0) {
+            for (int q = 0; q < 3; ++q) k[q] = bn.nyq[q] ? M(0) : M(bn.m[q]);
+            const M ksq = k[0] * k[0] + k[1] * k[1] + k[2] * k[2];
+            if (ksq != M(0)) {
+                M mult = M(1);
+                if (r.incomp == 2) {
+                    const M inner = M(r.beta) * (M(1) / ksq + M(1));
+                    mult = M(1) / (M(r.alpha) / inner + M(1));
+                }
+                mfac = mult / ksq;
+            }
+        }
+        M dr = M(0), di = M(0);
+        for (int c = 0; c < g.d; ++c) {
+            const M kc = k[g.comp_axis(c)];
+            dr += kc * br[c];
+            di += kc * bi[c];
+        }
+        const M iN = M(invN);
+        for (int c = 0; c < g.d; ++c) {
+            const M kc = k[g.comp_axis(c)];
+            M orr = (br[c] - kc * mfac * dr) * iN;
+            M oi = (bi[c] - kc * mfac * di) * iN;
+            if (have_a) {
+                C av = a[(long long)c * cnt + e];
+                orr += sa * av.x;
+                oi += sa * av.y;
+            }
+            C o;
+            o.x = orr;
+            o.y = oi;
+            a[(long long)c * cnt + e] = o;
+        }
+    }
+}
+
+static int slab_blocks(long long cnt) { return (int)std::min<long long>((cnt + 255) / 256, 148LL * 16); }
+
+void slab_spec_scale(const Dims& g, int i1_off, int n1_loc, int dtype, int ncomp, void* x, int kind,
+                     const RegSpec& r, cudaStream_t st) {
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
+    if (dtype == F64)
+        k_slab_spec_scale<cufftDoubleComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, i1_off, n1_loc, ncomp,
+                                                                              (cufftDoubleComplex*)x, kind, r, invN);
+    else
+        k_slab_spec_scale<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, i1_off, n1_loc, ncomp, (cufftComplex*)x,
+                                                                        kind, r, invN);
+    FRG_CHECK_LAUNCH();
+}
+
+void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a, const void* b, const RegSpec& r,
+                       bool project, cudaStream_t st) {
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
+    if (dtype == F64)
+        k_slab_combine<cufftDoubleComplex><<<slab_blocks(cnt), 256, 0, st>>>(
+            g, i1_off, n1_loc, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, r, invN, a != b, project);
+    else
+        k_slab_combine<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, i1_off, n1_loc, (cufftComplex*)a,
+                                                                     (const cufftComplex*)b, r, invN, a != b, project);
+    FRG_CHECK_LAUNCH();
+}
+
+}  // namespace frg

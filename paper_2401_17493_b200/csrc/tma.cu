@@ -25,7 +25,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
     FRG_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA field must be 16-byte aligned");
-    const cuuint64_t dims[2] = {(cuuint64_t)g.n2, (cuuint64_t)g.n0 * g.n1};
+    const cuuint64_t dims[2] = {(cuuint64_t)g.n2, (cuuint64_t)(g.n0 + 2 * g.h0) * g.n1};
     const cuuint64_t strides[1] = {(cuuint64_t)g.n2 * 4};
     const cuuint32_t box[2] = {TB_K, TB_J};
     const cuuint32_t estr[2] = {1, 1};

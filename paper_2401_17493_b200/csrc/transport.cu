@@ -69,14 +69,15 @@ void sample_q(const void* vals, int dtype, const Dims& g, const double* q0, cons
 template <typename T, typename VI, int D>
 struct DepartureOp {
     using V = VI;
-    const VI* v[3];      // per component
+    const VI* v[3];      // per component: gathered source (slab: with ghost planes)
+    const VI* vl[3];     // per component: v at the output voxels
     T sc[3];             // per component: h_t / h_axis
     T* out[3];           // per component
     int axis_of[3];
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const {
         T dd[3] = {T(0), T(0), T(0)};
 #pragma unroll
-        for (int c = 0; c < D; ++c) dd[axis_of[c]] = sc[c] * (T)v[c][p];
+        for (int c = 0; c < D; ++c) dd[axis_of[c]] = sc[c] * (T)vl[c][p];
         d0 = dd[0];
         d1 = dd[1];
         d2 = dd[2];
@@ -84,39 +85,44 @@ struct DepartureOp {
     __host__ __device__ __forceinline__ const VI* field(int f) const { return v[f]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
 #pragma unroll
-        for (int c = 0; c < D; ++c) out[c][p] = (T(0.5) * sc[c]) * ((T)v[c][p] + vals[c]);
+        for (int c = 0; c < D; ++c) out[c][p] = (T(0.5) * sc[c]) * ((T)vl[c][p] + vals[c]);
     }
 };
 
 template <typename T, typename VI, int D>
-static void departure_d(const Dims& g, int method, double ht, const VI* v, T* disp, cudaStream_t st) {
+static void departure_d(const Dims& g, int method, double ht, const VI* v, const VI* vloc, T* disp,
+                        cudaStream_t st) {
     DepartureOp<T, VI, D> op;
+    const size_t Ns = (size_t)(g.n0 + 2 * g.h0) * g.n1 * g.n2;  // source component stride
     for (int c = 0; c < D; ++c) {
         int a = g.comp_axis(c);
-        op.v[c] = v + (size_t)c * g.N;
+        op.v[c] = v + (size_t)c * Ns;
+        op.vl[c] = vloc + (size_t)c * g.N;
         op.out[c] = disp + (size_t)c * g.N;
-        op.sc[c] = (T)(ht / (TWO_PI / g.axis_len(a)));
+        op.sc[c] = (T)(ht / (TWO_PI / g.axis_glob(a)));
         op.axis_of[c] = a;
     }
     launch_sl<T, D>(g, method, op, st);
 }
 
 template <typename T, typename VI>
-static void departure_t(const Dims& g, int method, double ht, const VI* v, T* disp, cudaStream_t st) {
+static void departure_t(const Dims& g, int method, double ht, const VI* v, const VI* vloc, T* disp,
+                        cudaStream_t st) {
     if (g.d == 3)
-        departure_d<T, VI, 3>(g, method, ht, v, disp, st);
+        departure_d<T, VI, 3>(g, method, ht, v, vloc, disp, st);
     else
-        departure_d<T, VI, 2>(g, method, ht, v, disp, st);
+        departure_d<T, VI, 2>(g, method, ht, v, vloc, disp, st);
 }
 
 void departure(const Dims& g, int tdtype, int vdtype, int method, double h_t, const void* v, void* disp,
-               cudaStream_t st) {
+               cudaStream_t st, const void* vloc) {
+    if (!vloc) vloc = v;
     if (tdtype == F64 && vdtype == F64)
-        departure_t(g, method, h_t, (const double*)v, (double*)disp, st);
+        departure_t(g, method, h_t, (const double*)v, (const double*)vloc, (double*)disp, st);
     else if (tdtype == F32 && vdtype == F32)
-        departure_t(g, method, h_t, (const float*)v, (float*)disp, st);
+        departure_t(g, method, h_t, (const float*)v, (const float*)vloc, (float*)disp, st);
     else if (tdtype == F32 && vdtype == F64)
-        departure_t(g, method, h_t, (const double*)v, (float*)disp, st);
+        departure_t(g, method, h_t, (const double*)v, (const double*)vloc, (float*)disp, st);
     else
         throw Error(E_ARG, "departure: unsupported dtype combination");
 }
@@ -226,13 +232,14 @@ template <typename T>
 struct AdjMultOp {
     using V = T;
     DispSrc<T> ds;
-    const T* divv;
+    const T* divv;  // gathered source (slab: with ghost planes)
+    const T* divl;  // div v at the output voxels
     T* cmul;
     T ht;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int) const { return divv; }
     using Pre = T;
-    __device__ __forceinline__ T pre(int p) const { return divv[p]; }
+    __device__ __forceinline__ T pre(int p) const { return divl[p]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[1], T b) const {
         T a = vals[0];
         cmul[p] = T(1) + T(0.5) * ht * (a + b + ht * a * b);
@@ -255,21 +262,24 @@ struct AdjStepOp {
 
 template <typename T>
 static void adjoint_multiplier_t(const Dims& g, int method, double ht, const T* disp_b, const T* divv, T* cmul,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const T* divl) {
     AdjMultOp<T> op;
     op.ds = disp_src(g, disp_b);
     op.divv = divv;
+    op.divl = divl ? divl : divv;
     op.cmul = cmul;
     op.ht = (T)ht;
     launch_sl<T, 1>(g, method, op, st);
 }
 
 void adjoint_multiplier(const Dims& g, int tdtype, int method, double h_t, const void* disp_b, const void* divv,
-                        void* cmul, cudaStream_t st) {
+                        void* cmul, cudaStream_t st, const void* divl) {
     if (tdtype == F64)
-        adjoint_multiplier_t(g, method, h_t, (const double*)disp_b, (const double*)divv, (double*)cmul, st);
+        adjoint_multiplier_t(g, method, h_t, (const double*)disp_b, (const double*)divv, (double*)cmul, st,
+                             (const double*)divl);
     else
-        adjoint_multiplier_t(g, method, h_t, (const float*)disp_b, (const float*)divv, (float*)cmul, st);
+        adjoint_multiplier_t(g, method, h_t, (const float*)disp_b, (const float*)divv, (float*)cmul, st,
+                             (const float*)divl);
 }
 
 template <typename T>

@@ -19,7 +19,8 @@ template <typename T, int D>
 struct IncFirstOp {
     using V = T;
     DispSrc<T> ds;
-    const T* vtT[D];
+    const T* vtT[D];  // gathered source (slab: with ghost planes)
+    const T* vl[D];   // v~ at the output voxels
     const T* gy;  // n_t x D x N, grad m_j at y
     const T* gx;  // (n_t + 1) x D x N, grad m_j at x
     size_t N;
@@ -40,7 +41,7 @@ struct IncFirstOp {
 #pragma unroll
         for (int u = 0; u < TI; ++u)
 #pragma unroll
-            for (int c = 0; c < D; ++c) vx[u][c] = ok[u] ? __ldg(vtT[c] + p0 + u * pstride) : T(0);
+            for (int c = 0; c < D; ++c) vx[u][c] = ok[u] ? __ldg(vl[c] + p0 + u * pstride) : T(0);
         for (int j = 0; j < n_t; ++j) {
             const T* __restrict__ gyj = gy + (size_t)j * D * N + p0;
             const T* __restrict__ gxj = gx + (size_t)(j + 1) * D * N + p0;
@@ -73,7 +74,7 @@ struct IncFirstOp {
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
         T vx[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) vx[c] = vtT[c][p];
+        for (int c = 0; c < D; ++c) vx[c] = vl[c][p];
         for (int j = 0; j < n_t; ++j) {
             T f0 = T(0), f1 = T(0);
 #pragma unroll
@@ -131,7 +132,10 @@ static void inc_state_d(const Dims& g, int method, int n_t, const T* disp, const
     {
         IncFirstOp<T, D> op;
         op.ds = disp_src(g, disp);
-        for (int c = 0; c < D; ++c) op.vtT[c] = vsrc + c * N;
+        for (int c = 0; c < D; ++c) {
+            op.vtT[c] = vsrc + c * N;
+            op.vl[c] = vsrc + c * N;
+        }
         op.gy = grads_y;
         op.gx = grads;
         op.N = N;
@@ -154,6 +158,40 @@ static void inc_state_d(const Dims& g, int method, int n_t, const T* disp, const
         op.fsign = fsign;
         launch_sl<T, 1>(g, method, op, st);
     }
+}
+
+void inc_first(const Dims& g, int method, int n_t, const float* disp, const float* grads, const float* grads_y,
+               const float* vt_src, const float* vt_loc, float* m1, float* S, cudaStream_t st) {
+    FRG_REQUIRE(g.d == 3, "slab transport is 3D");
+    const size_t Ns = (size_t)(g.n0 + 2 * g.h0) * g.n1 * g.n2;
+    IncFirstOp<float, 3> op;
+    op.ds = disp_src(g, disp);
+    for (int c = 0; c < 3; ++c) {
+        op.vtT[c] = vt_src + c * Ns;
+        op.vl[c] = vt_loc + c * g.N;
+    }
+    op.gy = grads_y;
+    op.gx = grads;
+    op.N = g.N;
+    op.n_t = n_t;
+    op.m1 = m1;
+    op.fin = nullptr;
+    op.S = S;
+    op.fsign = 0.f;
+    op.hh = 0.5f * (float)(1.0 / n_t);
+    launch_sl<float, 3>(g, method, op, st);
+}
+
+void inc_step(const Dims& g, int method, const float* disp, const float* m_src, const float* Sj, float* m_next,
+              cudaStream_t st) {
+    IncStepOp<float> op;
+    op.ds = disp_src(g, disp);
+    op.mj = m_src;
+    op.Sj = Sj;
+    op.mnext = m_next;
+    op.fin = nullptr;
+    op.fsign = 0.f;
+    launch_sl<float, 1>(g, method, op, st);
 }
 
 template <typename T, typename CV>

@@ -1,0 +1,487 @@
+"""Slab-decomposed multi-GPU GN-Krylov core.
+
+The reference package is single-process (pkg/src/flowreg has no MPI/NCCL);
+CLAIRE's distributed design is described in PAPER.md:500-545: slabs along
+the slowest axis, FFT transposes by all-to-all, off-rank departure points.
+This module is that layer for one node of B200s, one process per GPU:
+
+* rank r owns planes [r n0/P, (r+1) n0/P) of every field (axis 0, the
+  slowest C-order axis = the paper's x1);
+* SL steps and FD8 read GHOST PLANES: before each gather the source field's
+  W nearest planes are exchanged with the two ring neighbours
+  (``SlabComm.halo``: NCCL send/recv), W = ceil(max |disp_0|) + 2 for cubic,
+  computed once per displacement map and max-reduced over ranks, then the
+  fp32 TMA gather kernel runs on the owned planes with h0 = W (no axis-0
+  wrap).  This replaces the reference-free "route every off-rank departure
+  point" scheme by a CFL-bounded halo: the same bytes at the CFL numbers of
+  registration velocities, and no per-point bookkeeping;
+* spectral operators run as batched 2D R2C over the owned planes, a packed
+  all-to-all to an axis-1 split, a batched 1D C2C along axis 0, the fused
+  pointwise operator with global frequencies, and the inverse chain
+  (``SlabFFT``);
+* reductions are local fused kernels + one all-reduce of a scalar.
+
+Host control (PCG / Armijo / Newton) is replicated SPMD: every rank runs the
+same ``optimizer`` code on identical all-reduced scalars
+(``dist_register``).  The exchange uses torch.distributed — NCCL on the GPU
+box; with the gloo backend (CPU tests, or several ranks sharing one GPU)
+buffers are staged through host memory.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+from . import _lib as L
+from .diffops import frg_reg
+from .kkt import PrecondKind, RegConfig
+
+__all__ = ["SlabComm", "SlabGrid", "SlabFFT", "DistKktState", "dist_register", "slab_bounds", "halo_width"]
+
+TWO_PI = 2.0 * math.pi
+
+
+def slab_bounds(n0: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Owned plane range [lo, hi) of ``rank`` (n0 must split evenly)."""
+    if n0 % nranks != 0:
+        raise ValueError(f"n0 = {n0} does not split over {nranks} ranks")
+    m = n0 // nranks
+    return rank * m, (rank + 1) * m
+
+
+def halo_width(max_abs_disp0: float, method: str = "cubic") -> int:
+    """Ghost planes a gather needs for axis-0 displacements |d0| <= max_abs_disp0
+    (index units): stencil planes floor(d0) - 1 .. floor(d0) + 2 for cubic,
+    floor(d0) .. floor(d0) + 1 for linear."""
+    extra = 2 if method == "cubic" else 1
+    return int(math.ceil(max(float(max_abs_disp0), 0.0))) + extra
+
+
+class SlabComm:
+    """Ring / all-to-all / all-reduce exchanges of the slab decomposition.
+
+    NCCL moves device tensors directly; any other backend stages through
+    host memory (gloo tests, several ranks on one GPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = tdist.get_rank(group)
+        self.size = tdist.get_world_size(group)
+        self.staged = tdist.get_backend(group) != "nccl"
+
+    # -- scalars -----------------------------------------------------------
+    def all_reduce(self, value: float, op: str = "sum") -> float:
+        if self.size == 1:
+            return float(value)
+        dev = "cpu" if self.staged else torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM if op == "sum" else tdist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    # -- all-to-all with equal chunks along dim 0 -------------------------
+    def all_to_all(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        if self.size == 1:
+            out.copy_(inp)
+            return
+        if self.staged:
+            o = torch.empty(out.shape, dtype=out.dtype)
+            tdist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+        else:
+            tdist.all_to_all_single(out, inp, group=self.group)
+
+    # -- ghost planes ----------------------------------------------------
+    def halo(self, ext: torch.Tensor, W: int) -> None:
+        """ext (C, n0_loc + 2W, n1, n2) with the owned planes at [W, W + n0_loc):
+        fill the W ghost planes on each side from the periodic ring neighbours."""
+        if W == 0:
+            return
+        n0l = ext.shape[1] - 2 * W
+        if W > n0l and self.size > 1:
+            raise ValueError(f"halo of {W} planes exceeds the {n0l}-plane slab; use fewer ranks")
+        if self.size == 1:
+            ext[:, :W].copy_(ext[:, n0l:n0l + W])
+            ext[:, n0l + W:].copy_(ext[:, W:2 * W])
+            return
+        prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
+        send_lo = ext[:, W:2 * W].contiguous()          # my first planes -> prev's upper ghosts
+        send_hi = ext[:, n0l:n0l + W].contiguous()      # my last planes  -> next's lower ghosts
+        recv_hi = torch.empty_like(send_lo)
+        recv_lo = torch.empty_like(send_hi)
+        if self.staged:
+            send_lo, send_hi = send_lo.cpu(), send_hi.cpu()
+            recv_hi, recv_lo = recv_hi.cpu(), recv_lo.cpu()
+        # identical op order on every rank: with P = 2 both messages share a
+        # peer and match in issue order (send_lo <-> recv_hi, send_hi <-> recv_lo)
+        ops = [tdist.P2POp(tdist.isend, send_lo, prev, self.group),
+               tdist.P2POp(tdist.irecv, recv_hi, nxt, self.group),
+               tdist.P2POp(tdist.isend, send_hi, nxt, self.group),
+               tdist.P2POp(tdist.irecv, recv_lo, prev, self.group)]
+        for req in tdist.batch_isend_irecv(ops):
+            req.wait()
+        ext[:, :W].copy_(recv_lo)
+        ext[:, n0l + W:].copy_(recv_hi)
+
+
+@dataclass(frozen=True)
+class SlabGrid:
+    """Global grid + this rank's slab.  Quacks like fields.Grid for the host
+    control code (cell_volume, d, n_t, dtype; ``n`` is the LOCAL shape)."""
+
+    n_glob: tuple
+    rank: int
+    size: int
+    n_t: int = 4
+    dtype: np.dtype = np.dtype(np.float64)
+
+    @property
+    def lo(self) -> int:
+        return slab_bounds(self.n_glob[0], self.size, self.rank)[0]
+
+    @property
+    def n0_loc(self) -> int:
+        return self.n_glob[0] // self.size
+
+    @property
+    def n(self) -> tuple:
+        return (self.n0_loc, self.n_glob[1], self.n_glob[2])
+
+    @property
+    def d(self) -> int:
+        return 3
+
+    @property
+    def h(self) -> tuple:
+        return tuple(TWO_PI / ni for ni in self.n_glob)
+
+    @property
+    def h_t(self) -> float:
+        return 1.0 / self.n_t
+
+    @property
+    def cell_volume(self) -> float:
+        return float(np.prod(self.h))
+
+    @property
+    def torch_dtype(self):
+        return torch.float64 if np.dtype(self.dtype) == np.float64 else torch.float32
+
+
+def _c(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class SlabFFT:
+    """Distributed real FFT of slab fields (see module docstring)."""
+
+    def __init__(self, grid: SlabGrid, comm: SlabComm):
+        n0, n1, n2 = grid.n_glob
+        if n0 % comm.size or n1 % comm.size:
+            raise ValueError("n0 and n1 must both split over the ranks")
+        self.g, self.comm = grid, comm
+        self.nh = n2 // 2 + 1
+        self.n1l = n1 // comm.size
+        self.i1_off = comm.rank * self.n1l
+        self.nloc = L.n3(grid.n)
+        self.nglob = L.n3(grid.n_glob)
+
+    def spectrum(self, ncomp: int, dtype: torch.dtype) -> torch.Tensor:
+        cdt = torch.complex128 if dtype == torch.float64 else torch.complex64
+        return torch.empty((ncomp, self.g.n_glob[0], self.n1l, self.nh), dtype=cdt, device="cuda")
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x real (C, n0_loc, n1, n2) -> axis-1 split spectrum (C, n0, n1/P, nh)."""
+        C = x.shape[0]
+        dt = L.dtype_code(x.dtype)
+        cdt = torch.complex128 if x.dtype == torch.float64 else torch.complex64
+        n0l, n1, _ = self.g.n
+        P = self.comm.size
+        y = torch.empty((C, n0l, n1, self.nh), dtype=cdt, device="cuda")
+        L.check(L.lib().frg_slab_fft2(self.nloc, dt, C, 1, _c(x), _c(y), L.stream()), "slab_fft2")
+        packed = torch.empty((C, P, n0l, self.n1l, self.nh), dtype=cdt, device="cuda")
+        L.check(L.lib().frg_slab_transpose(1, P, self.nloc, dt, C, _c(y), _c(packed), L.stream()), "slab_transpose")
+        spec = self.spectrum(C, x.dtype)
+        for c in range(C):
+            self.comm.all_to_all(spec[c].view(P, n0l, self.n1l, self.nh), packed[c])
+        L.check(L.lib().frg_slab_fft1(self.g.n_glob[0], self.n1l, self.g.n_glob[2], dt, C, 1, _c(spec), L.stream()),
+                "slab_fft1")
+        return spec
+
+    def inverse(self, spec: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """(C, n0, n1/P, nh) -> real (C, n0_loc, n1, n2), unnormalised; spec is consumed."""
+        C = spec.shape[0]
+        dt = L.dtype_code(out.dtype)
+        n0l, n1, _ = self.g.n
+        P = self.comm.size
+        L.check(L.lib().frg_slab_fft1(self.g.n_glob[0], self.n1l, self.g.n_glob[2], dt, C, -1, _c(spec), L.stream()),
+                "slab_fft1")
+        packed = torch.empty((C, P, n0l, self.n1l, self.nh), dtype=spec.dtype, device="cuda")
+        for c in range(C):
+            self.comm.all_to_all(packed[c], spec[c].view(P, n0l, self.n1l, self.nh))
+        y = torch.empty((C, n0l, n1, self.nh), dtype=spec.dtype, device="cuda")
+        L.check(L.lib().frg_slab_transpose(-1, P, self.nloc, dt, C, _c(packed), _c(y), L.stream()), "slab_transpose")
+        L.check(L.lib().frg_slab_fft2(self.nloc, dt, C, -1, _c(y), _c(out), L.stream()), "slab_fft2")
+        return out
+
+    def apply(self, x: torch.Tensor, kind: str, reg, out: torch.Tensor | None = None) -> torch.Tensor:
+        """real(ifft(symbol * fft(x))) for the symbols of frg_slab_spec_apply."""
+        spec = self.forward(x)
+        L.check(L.lib().frg_slab_spec_apply(self.nglob, self.i1_off, self.n1l, L.dtype_code(x.dtype), x.shape[0],
+                                            _c(spec), L.SYM[kind], ctypes.byref(reg), L.stream()), "slab_spec_apply")
+        out = torch.empty_like(x) if out is None else out
+        return self.inverse(spec, out)
+
+    def reg_plus_project(self, a: torch.Tensor | None, b: torch.Tensor, reg, project: bool,
+                         out: torch.Tensor) -> torch.Tensor:
+        """out = alpha L a + P(b) (a may be None: P(b) only); a, b, out same dtype."""
+        sb = self.forward(b)
+        sa = self.forward(a) if a is not None else sb
+        L.check(L.lib().frg_slab_spec_combine(self.nglob, self.i1_off, self.n1l, L.dtype_code(b.dtype), _c(sa),
+                                              _c(sb), ctypes.byref(reg), int(project), L.stream()),
+                "slab_spec_combine")
+        return self.inverse(sa, out)
+
+
+class _Vec:
+    """Minimal VectorField stand-in for the host control code (.grid, .data)."""
+
+    __slots__ = ("grid", "data")
+
+    def __init__(self, grid, data):
+        self.grid, self.data = grid, data
+
+
+class DistKktState:
+    """Slab-decomposed counterpart of kkt.KktState (kkt.py:136-341) for SSD,
+    FD8, linear / cubic fp32 transport, fp64 control vectors.
+
+    Same methods and counters as KktState (refresh, gradient, hessian_matvec,
+    apply_precond('reg'), objective, objective_at, mismatch), each a sequence
+    of per-rank slab kernels and exchanges; all ranks call them in lockstep."""
+
+    def __init__(self, m0: torch.Tensor, m1: torch.Tensor, reg: RegConfig, comm: SlabComm, n_glob, n_t: int = 4,
+                 method: str = "cubic", v_init: torch.Tensor | None = None):
+        if method not in ("linear", "cubic"):
+            raise ValueError("slab transport supports linear / cubic interpolation")
+        self.comm = comm
+        self.grid = SlabGrid(tuple(int(v) for v in n_glob), comm.rank, comm.size, n_t=n_t)
+        self.reg = reg
+        self.method = method
+        self._m = L.METHODS[method]
+        self._reg = frg_reg(reg.operator, reg.alpha, reg.incomp)
+        self._project = reg.incomp.mode != "none"
+        # H1: spectral part in fp32 (as the single-GPU fast path); H2/H3 fp64
+        self._spec_dt = torch.float32 if reg.operator.order == 1 else torch.float64
+        self.fft = SlabFFT(self.grid, comm)
+        g = self.grid
+        self.n_loc = L.n3(g.n)
+        self.N = int(np.prod(g.n))
+        self.m0 = m0.to(device="cuda", dtype=torch.float32).contiguous()
+        self.m1 = m1.to(device="cuda", dtype=torch.float32).contiguous()
+        if tuple(self.m0.shape) != g.n or tuple(self.m1.shape) != g.n:
+            raise ValueError(f"slab images must be {g.n}")
+        self.matvecs = 0
+        self.pde_solves = 0
+        self.precond_fallbacks = 0
+        self._init_mismatch = self._ssd(self.m0)
+        v0 = torch.zeros((3, *g.n), dtype=torch.float64, device="cuda") if v_init is None else v_init
+        self.refresh(v0)
+
+    # -- helpers -----------------------------------------------------------
+    def _ext(self, x: torch.Tensor, W: int) -> torch.Tensor:
+        """(C, n0_loc, n1, n2) -> (C, n0_loc + 2W, n1, n2) with exchanged ghost planes."""
+        x = x if x.dim() == 4 else x.unsqueeze(0)
+        C, n0l = x.shape[0], x.shape[1]
+        ext = torch.empty((C, n0l + 2 * W, *x.shape[2:]), dtype=x.dtype, device=x.device)
+        ext[:, W:W + n0l].copy_(x)
+        self.comm.halo(ext, W)
+        return ext
+
+    def _halo_of(self, disp: torch.Tensor) -> int:
+        local = float(disp[0].abs().max().item())
+        return max(halo_width(self.comm.all_reduce(local, "max"), self.method), 1)
+
+    def dot(self, a: torch.Tensor, b: torch.Tensor) -> float:
+        """Global sum(a * b) (unweighted), fused local kernel + all-reduce."""
+        out = ctypes.c_double()
+        L.check(L.lib().frg_dot(L.dtype_code(a.dtype), L.ptr(a), L.ptr(b), a.numel(), ctypes.byref(out), L.stream()),
+                "dot")
+        return self.comm.all_reduce(out.value)
+
+    def norm_inf(self, a: torch.Tensor) -> float:
+        out = ctypes.c_double()
+        L.check(L.lib().frg_norm_inf(L.dtype_code(a.dtype), L.ptr(a), a.numel(), ctypes.byref(out), L.stream()),
+                "norm_inf")
+        return self.comm.all_reduce(out.value, "max")
+
+    def _ssd(self, md: torch.Tensor) -> float:
+        r = md - self.m1
+        return 0.5 * self.dot(r, r) * self.grid.cell_volume
+
+    def _gather(self, disp, W, srcs, outs):
+        ins = (ctypes.c_void_p * len(srcs))(*[s.data_ptr() for s in srcs])
+        ous = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        L.check(L.lib().frg_slab_gather(self.n_loc, self.grid.n_glob[0], W, self._m, _c(disp), len(srcs), ins, ous,
+                                        L.stream()), "slab_gather")
+
+    def _departure(self, v32: torch.Tensor, sign: float) -> torch.Tensor:
+        vs = v32 if sign > 0 else -v32
+        h0 = TWO_PI / self.grid.n_glob[0]
+        Wv = max(halo_width(self.comm.all_reduce(float(vs[0].abs().max().item()) * self.grid.h_t / h0, "max"),
+                            self.method), 4)
+        v_ext = self._ext(vs, Wv)
+        disp = torch.empty_like(vs)
+        L.check(L.lib().frg_slab_departure(self.n_loc, self.grid.n_glob[0], Wv, self._m, self.grid.h_t, _c(v_ext),
+                                           _c(vs), _c(disp), L.stream()), "slab_departure")
+        return disp, v_ext, Wv
+
+    def _state_solve(self, disp, W, keep: bool):
+        g = self.grid
+        m = self.m0
+        series = [m] if keep else None
+        for _ in range(g.n_t):
+            nxt = torch.empty_like(m)
+            self._gather(disp, W, [self._ext(m, W)], [nxt])
+            m = nxt
+            if keep:
+                series.append(m)
+        return series if keep else m
+
+    def _spectral_out(self, a64: torch.Tensor | None, b32: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """out (fp64) = alpha L a + P(b) in the spectral precision."""
+        sdt = self._spec_dt
+        a = a64.to(sdt) if a64 is not None else None
+        res = torch.empty(b32.shape, dtype=sdt, device="cuda")
+        self.fft.reg_plus_project(a, b32.to(sdt), self._reg, self._project, res)
+        out.copy_(res)
+        return out
+
+    def _body_force(self, lam):
+        g = self.grid
+        b = torch.empty((3, *g.n), dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_body_force(self.n_loc, 3, L.F32, g.n_t, _c(lam), _c(self.grads), _c(b), L.stream()),
+                "body_force")
+        return b
+
+    # -- KktState surface ------------------------------------------------
+    def refresh(self, v: torch.Tensor) -> None:
+        """kkt.py:166-186 on the slab."""
+        g = self.grid
+        self.v = _Vec(g, v.to(device="cuda", dtype=torch.float64).contiguous())
+        v32 = self.v.data.float()
+        self.disp_f, v_ext, Wv = self._departure(v32, 1.0)
+        self.disp_b, _, _ = self._departure(v32, -1.0)
+        self.Wf, self.Wb = self._halo_of(self.disp_f), self._halo_of(self.disp_b)
+        divv = torch.empty(g.n, dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_slab_fd8_divergence(self.n_loc, g.n_glob[0], Wv, _c(v_ext), _c(divv), L.stream()),
+                "slab_fd8_divergence")
+        self.mseries = self._state_solve(self.disp_f, self.Wf, keep=True)
+        Wg = max(self.Wf, 4)
+        self.grads = torch.empty((g.n_t + 1, 3, *g.n), dtype=torch.float32, device="cuda")
+        for j, mj in enumerate(self.mseries):
+            L.check(L.lib().frg_slab_fd8_gradient(self.n_loc, g.n_glob[0], Wg, 1, _c(self._ext(mj, Wg)),
+                                                  _c(self.grads[j]), L.stream()), "slab_fd8_gradient")
+        self.grads_y = torch.empty((g.n_t, 3, *g.n), dtype=torch.float32, device="cuda")
+        for j in range(g.n_t):
+            ext = self._ext(self.grads[j], self.Wf)
+            self._gather(self.disp_f, self.Wf, [ext[c] for c in range(3)], [self.grads_y[j, c] for c in range(3)])
+        self.cmul = torch.empty(g.n, dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_slab_adjoint_multiplier(self.n_loc, g.n_glob[0], self.Wb, self._m, g.h_t,
+                                                    _c(self.disp_b), _c(self._ext(divv, self.Wb)), _c(divv),
+                                                    _c(self.cmul), L.stream()), "slab_adjoint_multiplier")
+        self.lam = torch.empty((g.n_t + 1, *g.n), dtype=torch.float32, device="cuda")
+        torch.sub(self.m1, self.mseries[-1], out=self.lam[g.n_t])  # -(m(1) - m1), SSD
+        self._adjoint(self.lam)
+        self.pde_solves += 2
+        self._dist = None
+
+    def _adjoint(self, series):
+        g = self.grid
+        for j in range(g.n_t, 0, -1):
+            L.check(L.lib().frg_slab_adjoint_step(self.n_loc, g.n_glob[0], self.Wb, self._m, _c(self.disp_b),
+                                                  _c(self.cmul), _c(self._ext(series[j], self.Wb)),
+                                                  _c(series[j - 1]), L.stream()), "slab_adjoint_step")
+
+    def gradient(self) -> _Vec:
+        out = torch.empty((3, *self.grid.n), dtype=torch.float64, device="cuda")
+        self._spectral_out(self.v.data, self._body_force(self.lam), out)
+        return _Vec(self.grid, out)
+
+    def hessian_matvec(self, vtilde, out: torch.Tensor | None = None) -> _Vec:
+        """kkt.py:237-260 (GN, SSD) on the slab."""
+        g = self.grid
+        vt = vtilde.data if hasattr(vtilde, "data") else vtilde
+        vtT = vt.float()
+        mt = torch.empty((g.n_t + 1, *g.n), dtype=torch.float32, device="cuda")
+        S = torch.empty((max(g.n_t - 1, 1), *g.n), dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_slab_inc_first(self.n_loc, g.n_glob[0], self.Wf, self._m, g.n_t, _c(self.disp_f),
+                                           _c(self.grads), _c(self.grads_y), _c(self._ext(vtT, self.Wf)), _c(vtT),
+                                           _c(mt[1]), _c(S), L.stream()), "slab_inc_first")
+        for j in range(1, g.n_t):
+            L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], self.Wf, self._m, _c(self.disp_f),
+                                              _c(self._ext(mt[j], self.Wf)), _c(S[j - 1]), _c(mt[j + 1]),
+                                              L.stream()), "slab_inc_step")
+        lt = torch.empty_like(mt)
+        torch.neg(mt[g.n_t], out=lt[g.n_t])  # SSD: lam~(1) = -m~(1)
+        self._adjoint(lt)
+        self.matvecs += 1
+        self.pde_solves += 2
+        out = torch.empty((3, *g.n), dtype=torch.float64, device="cuda") if out is None else out
+        self._spectral_out(vt, self._body_force(lt), out)
+        return _Vec(g, out)
+
+    def apply_precond(self, r, kind: PrecondKind | None = None, outer_tol: float = 0.0,
+                      out: torch.Tensor | None = None) -> _Vec:
+        """kkt.py:308-311 ('reg': the spectral inverse of alpha L)."""
+        if kind is not None and kind.kind != "reg":
+            raise ValueError("the slab path implements the 'reg' preconditioner")
+        rd = r.data if hasattr(r, "data") else r
+        res = self.fft.apply(rd.to(self._spec_dt), "reg_inv", self._reg)
+        out = torch.empty_like(rd) if out is None else out
+        out.copy_(res)
+        return _Vec(self.grid, out)
+
+    def _reg_energy(self, v64: torch.Tensor) -> float:
+        lv = self.fft.apply(v64.to(self._spec_dt), "reg", self._reg).to(torch.float64)
+        return 0.5 * self.dot(v64, lv) * self.grid.cell_volume
+
+    def objective(self) -> float:
+        if self._dist is None:
+            self._dist = self._ssd(self.mseries[-1])
+        return self._dist + self._reg_energy(self.v.data)
+
+    def objective_at(self, v_trial) -> float:
+        vt = (v_trial.data if hasattr(v_trial, "data") else v_trial).to(torch.float64)
+        disp, _, _ = self._departure(vt.float(), 1.0)
+        m = self._state_solve(disp, self._halo_of(disp), keep=False)
+        self.pde_solves += 1
+        return self._ssd(m) + self._reg_energy(vt)
+
+    def mismatch(self) -> float:
+        if self._init_mismatch == 0.0:
+            return 0.0
+        if self._dist is None:
+            self._dist = self._ssd(self.mseries[-1])
+        return self._dist / self._init_mismatch
+
+    def divergence_energy(self) -> float:
+        return 0.0
+
+    def detgrad_stats(self):
+        return 1.0, 1.0, 1.0
+
+
+def dist_register(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, config=None, reg: RegConfig | None = None,
+                  n_t: int = 4, method: str = "cubic", v0: torch.Tensor | None = None):
+    """optimizer.register (optimizer.py:174-281) on the slab decomposition:
+    the same host control, SPMD on every rank, reductions all-reduced."""
+    from .optimizer import OptimizerConfig, solve
+
+    reg = reg or RegConfig()
+    state = DistKktState(m0, m1, reg, comm, n_glob, n_t=n_t, method=method, v_init=v0)
+    return solve(state, config or OptimizerConfig(), PrecondKind("reg"), compute_detgrad=False)
