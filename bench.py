@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--precision", default="mixed", choices=["mixed", "f64", "f32"])
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-slab", action="store_true", help="skip the multi-GPU slab-decomposed C4 run (N > 1)")
+    ap.add_argument("--slab-n", type=int, default=512, help="grid of the slab-decomposed run (N > 1)")
     return ap.parse_args()
 
 
@@ -140,9 +142,16 @@ def run_b200(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU over NCCL; FRG_DIST_BACKEND=gloo lets several ranks share
+    # one GPU to exercise the multi-rank path (exchanges staged through host)
+    backend = os.environ.get("FRG_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2401_17493_b200 as F
     from paper_2401_17493_b200 import _lib as L
@@ -168,7 +177,7 @@ def run_b200(a):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -276,6 +285,13 @@ def run_b200(a):
                "includes": "KktState creation, all refresh/gradient/PCG/Armijo work and det(F) stats; "
                            "excludes synthetic-data generation"}
 
+    slab = None
+    if world > 1 and not a.no_slab:
+        try:
+            slab = run_slab(a, F, world, rank, barrier, max_over_ranks)
+        except Exception as exc:  # keep the headline line even if the slab run fails
+            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     if world > 1:
         dist.barrier()
     result = None
@@ -296,11 +312,54 @@ def run_b200(a):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if slab is not None:
+            result["slab"] = slab
         print(json.dumps(result))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def run_slab(a, F, world, rank, barrier, max_over_ranks):
+    """C4: ONE slab-decomposed registration problem across the N ranks
+    (dist.py: NCCL all-to-all FFT transposes + ghost-plane exchanges), GN
+    Hessian matvecs/s of that single problem (strong scaling)."""
+    import numpy as np
+    import torch
+
+    from paper_2401_17493_b200 import dist as D
+
+    n = a.slab_n
+    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3)
+    reg = F.RegConfig(alpha=1e-2, operator=F.RegOperatorSpec(1, True),
+                      incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    comm = D.SlabComm()
+    lo, hi = D.slab_bounds(n, world, rank)
+    v = (0.5 * vtrue.data[:, lo:hi]).contiguous()
+    st = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n), v_init=v)
+    del m0, m1, vtrue
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    vt = 0.1 * torch.randn((3, hi - lo, n, n), generator=gen, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(vt)
+    steps = max(3, min(a.steps, 10))
+    for _ in range(max(a.warmup, 3)):
+        st.hessian_matvec(vt, out=out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(steps):
+        st.hessian_matvec(vt, out=out)
+    s1.record()
+    torch.cuda.synchronize()
+    barrier()
+    t = max_over_ranks(s0.elapsed_time(s1)) / 1e3
+    return {"workload": f"C4: one {n}^3 GN Hessian matvec slab-decomposed over {world} ranks", "grid": [n] * 3,
+            "ranks": world, "value": steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps, "steps": steps,
+            "scaling": "strong", "halo_planes": [st.Wf, st.Wb],
+            "parallelism": f"slab along axis 0 x{world}: NCCL all-to-all FFT transposes, ghost-plane send/recv"}
 
 
 def cpu_baseline(a, m0, m1, vtrue, vt):
