@@ -38,6 +38,7 @@ extern "C" {
 #define FRG_NEAREST 0
 #define FRG_LINEAR 1
 #define FRG_CUBIC 2
+#define FRG_BSPLINE 3 /* cubic B-spline on spectrally prefiltered coefficients (no reference counterpart) */
 
 #define FRG_FD8 0
 #define FRG_SPECTRAL 1
@@ -57,6 +58,7 @@ extern "C" {
 #define FRG_SYM_LAPLACIAN 4    /*                                    diffops.py:142 */
 #define FRG_SYM_LOWPASS 5      /*                                    diffops.py:296 */
 #define FRG_SYM_HIGHPASS 6     /*                                    diffops.py:300 */
+#define FRG_SYM_BSPLINE_PREFILTER 7 /* 1 / prod_a (4 + 2 cos(2 pi m_a / n_a)) / 6 */
 
 #define FRG_PRECOND_REG 0
 #define FRG_PRECOND_H0 1

@@ -205,6 +205,50 @@ def sample_numpy(values, qs, method):
     return out.astype(values.dtype if values.dtype.kind == "f" else np.float64)
 
 
+# ---------------------------------------------------------------------------
+# cubic B-spline (north-star extension; NOT in the reference package, which
+# lists it out of scope at SPEC.md:302 — parity unpinned, checked by
+# properties: nodal exactness, polynomial/sine approximation order, and the
+# CUDA path against this restatement).  Gather structure of _kernels.py:191-219
+# with the uniform cubic B-spline weights; periodic interpolation condition
+# (c_{j-1} + 4 c_j + c_{j+1}) / 6 = u_j solved spectrally per axis.
+# ---------------------------------------------------------------------------
+def bspline_prefilter(values):
+    """Coefficients c with sum_a beta3 taps = values at every node (periodic)."""
+    v = np.asarray(values, dtype=np.float64)
+    sym = np.ones(v.shape)
+    for axis, n in enumerate(v.shape):
+        m = np.fft.fftfreq(n, 1.0 / n)
+        shape = [1] * v.ndim
+        shape[axis] = n
+        sym = sym * ((4.0 + 2.0 * np.cos(2.0 * np.pi * m / n)) / 6.0).reshape(shape)
+    return np.real(np.fft.ifftn(np.fft.fftn(v) / sym))
+
+
+def bspline_weights(t):
+    """beta3 at offsets -1, 0, 1, 2 for t in [0, 1)."""
+    return ((1.0 - t) ** 3 / 6.0, (3.0 * t ** 3 - 6.0 * t ** 2 + 4.0) / 6.0,
+            (-3.0 * t ** 3 + 3.0 * t ** 2 + 3.0 * t + 1.0) / 6.0, t ** 3 / 6.0)
+
+
+def sample_bspline(values, qs):
+    """Cubic B-spline interpolant of ``values`` at fractional indices qs (f64)."""
+    c = bspline_prefilter(values)
+    d, n = c.ndim, c.shape
+    fl = [np.floor(qs[i]) for i in range(d)]
+    w = [bspline_weights(qs[i] - fl[i]) for i in range(d)]
+    base = [fl[i].astype(np.int64) for i in range(d)]
+    out = np.zeros(np.asarray(qs[0]).shape)
+    for taps in np.ndindex(*(4,) * d):
+        ww = 1.0
+        idx = []
+        for i, a in enumerate(taps):
+            ww = ww * w[i][a]
+            idx.append((base[i] + a - 1) % n[i])
+        out = out + ww * c[tuple(idx)]
+    return out
+
+
 def interp_field(u, pts, method):
     """interp.interpolate / interpolate_vector (interp.py:42-62)."""
     n = u.shape[-len(pts):]

@@ -15,11 +15,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FRG_LIB", os.path.join(HERE, "libflowreg_b200.so"))
 
 F32, F64, I32 = 0, 1, 2
-METHODS = {"nearest": 0, "linear": 1, "cubic": 2}
+METHODS = {"nearest": 0, "linear": 1, "cubic": 2, "bspline": 3}
 SCHEMES = {"fd8": 0, "spectral": 1}
 DISTANCES = {"ssd": 0, "ncc": 1}
 INCOMP = {"none": 0, "incompressible": 1, "near-incompressible": 2}
-SYM = {"reg": 0, "reg_inv": 1, "reg_inv_sqrt": 2, "reg_kc": 3, "laplacian": 4, "lowpass": 5, "highpass": 6}
+SYM = {"reg": 0, "reg_inv": 1, "reg_inv_sqrt": 2, "reg_kc": 3, "laplacian": 4, "lowpass": 5, "highpass": 6,
+       "bspline_prefilter": 7}
 PRECOND = {"reg": 0, "h0": 1, "2level": 2}
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "non-finite data", -3: "CUDA error", -4: "cuFFT error",

@@ -34,7 +34,7 @@ static Dims dims_of(const int32_t n[3], int d) {
 }
 
 static void check_dtype(int dt) { FRG_REQUIRE(dt == FRG_F32 || dt == FRG_F64, "dtype must be FRG_F32 or FRG_F64"); }
-static void check_method(int m) { FRG_REQUIRE(m >= 0 && m <= 2, "unknown interpolation method"); }
+static void check_method(int m) { FRG_REQUIRE(m >= 0 && m <= 3, "unknown interpolation method"); }
 
 static RegSpec reg_of(const frg_reg* r) {
     FRG_REQUIRE(r != nullptr, "null frg_reg");
@@ -233,7 +233,7 @@ int frg_spectral_apply(const int32_t n[3], int32_t d, int32_t dtype, int32_t nco
                        int32_t symbol, const frg_reg* reg, void* stream) {
     return guard([&] {
         check_dtype(dtype);
-        FRG_REQUIRE(symbol >= 0 && symbol <= 6, "unknown spectral symbol");
+        FRG_REQUIRE(symbol >= 0 && symbol <= 7, "unknown spectral symbol");
         FRG_REQUIRE(ncomp >= 1, "ncomp must be >= 1");
         RegSpec r{1.0, 1, 1, 0, 1e-4};
         if (symbol <= FRG_SYM_REG_KC) r = reg_of(reg);
@@ -466,7 +466,7 @@ static Dims slab_dims(const int32_t n_loc[3], int32_t n0_glob, int32_t h0) {
     g.n0g = n0_glob;
     return g;
 }
-static void check_slab_method(int m) { FRG_REQUIRE(m == 1 || m == 2, "slab transport: linear or cubic"); }
+static void check_slab_method(int m) { FRG_REQUIRE(m == 1 || m == 2, "slab transport: linear or cubic (B-spline needs the global prefilter)"); }
 
 extern "C" {
 
@@ -570,7 +570,7 @@ int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc,
                         void* x, int32_t kind, const frg_reg* reg, void* stream) {
     return guard([&] {
         check_dtype(dtype);
-        FRG_REQUIRE(kind >= 0 && kind <= 6, "unknown symbol kind");
+        FRG_REQUIRE(kind >= 0 && kind <= 7, "unknown symbol kind");
         slab_spec_scale(dims_of(n_glob, 3), i1_off, n1_loc, dtype, ncomp, x, kind, reg_of(reg), ST(stream));
     });
 }

@@ -56,7 +56,10 @@ __host__ __device__ __forceinline__ int src_plane(const Dims& g, int b) {
     return r < 0 ? r + g.n0 : r;
 }
 
-enum Method { NEAREST = 0, LINEAR = 1, CUBIC = 2 };
+// BSPLINE: cubic B-spline on prefiltered coefficients (the caller's field is
+// prefiltered spectrally first, spectral.cu SK_BSPLINE_PREFILTER); same 4-tap
+// stencil geometry as CUBIC.
+enum Method { NEAREST = 0, LINEAR = 1, CUBIC = 2, BSPLINE = 3 };
 enum DType { F32 = 0, F64 = 1, I32 = 2 };
 
 struct Error : std::runtime_error {
@@ -130,6 +133,24 @@ __device__ __forceinline__ void lagrange4(T t, T w[4]) {
     w[3] = tp1 * t * tm1 * sixth;
 }
 
+// uniform cubic B-spline weights at offsets -1, 0, 1, 2 (t in [0, 1))
+template <typename T>
+__device__ __forceinline__ void bspline4(T t, T w[4]) {
+    const T sixth = T(1.0 / 6.0), omt = T(1) - t, t2 = t * t, t3 = t2 * t;
+    w[0] = omt * omt * omt * sixth;
+    w[1] = (T(3) * t3 - T(6) * t2 + T(4)) * sixth;
+    w[2] = (T(-3) * t3 + T(3) * t2 + T(3) * t + T(1)) * sixth;
+    w[3] = t3 * sixth;
+}
+
+template <typename T, int M>
+__device__ __forceinline__ void weights4(T t, T w[4]) {
+    if (M == BSPLINE)
+        bspline4(t, w);
+    else
+        lagrange4(t, w);
+}
+
 // Periodic wrap of an index that is usually inside [0, n) or within a few
 // periods of it: one unsigned compare on the common path, % only on wrap.
 __device__ __forceinline__ int wrap_near(int b, int n) {
@@ -151,7 +172,7 @@ struct Axis {
 
 template <int M>
 struct Taps {
-    static constexpr int value = (M == CUBIC ? 4 : (M == LINEAR ? 2 : 1));
+    static constexpr int value = ((M == CUBIC || M == BSPLINE) ? 4 : (M == LINEAR ? 2 : 1));
 };
 
 // Build the axis stencil for node `base` (any integer, wrapped here) and
@@ -171,7 +192,7 @@ __device__ __forceinline__ void axis_stencil(int base, T t, int n, int stride, A
         ax.w[1] = t;
     } else {
         T w[4];
-        lagrange4(t, w);
+        weights4<T, M>(t, w);
         if (n == 1) {
 #pragma unroll
             for (int a = 0; a < 4; ++a) {

@@ -74,7 +74,7 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
     FRG_REQUIRE(g.d == 2 || g.d == 3, "d must be 2 or 3");
     FRG_REQUIRE((g.d == 2) == (g.n0 == 1), "2D grids are passed as n = {1, n0, n1}");
     FRG_REQUIRE(n_t >= 1, "n_t must be >= 1");
-    FRG_REQUIRE(method >= 0 && method <= 2, "unknown interpolation method");
+    FRG_REQUIRE(method >= 0 && method <= 3, "unknown interpolation method");
     FRG_REQUIRE(scheme == 0 || scheme == 1, "unknown derivative scheme");
     FRG_REQUIRE(distance == 0 || distance == 1, "unknown distance measure");
     FRG_REQUIRE(tdt == F32 || tdt == F64, "transport dtype must be f32 or f64");

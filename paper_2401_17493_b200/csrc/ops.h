@@ -104,6 +104,7 @@ enum SpecKind {
     SK_LAPLACIAN = 4,    // -|k|^2
     SK_LOWPASS = 5,
     SK_HIGHPASS = 6,
+    SK_BSPLINE_PREFILTER = 7,  // 1 / prod_a (4 + 2 cos(2 pi m_a / n_a)) / 6 (cubic B-spline coefficients)
 };
 struct RegSpec {
     double alpha;

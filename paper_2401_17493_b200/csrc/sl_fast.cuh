@@ -277,6 +277,30 @@ __device__ __forceinline__ void lagrange4f_x2(float2 t, float2 (&w)[4]) {
     w[3] = __fmul2_rn(__fmul2_rn(p, tp1), make_float2(1.f / 6.f, 1.f / 6.f));
 }
 
+// cubic B-spline weights for two points (paired fp32), lane-for-lane equal to bspline4<float>
+__device__ __forceinline__ void bspline4f_x2(float2 t, float2 (&w)[4]) {
+    const float2 sixth = make_float2(1.f / 6.f, 1.f / 6.f);
+    const float2 omt = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-t.x, -t.y));
+    const float2 t2 = __fmul2_rn(t, t), t3 = __fmul2_rn(t2, t);
+    w[0] = __fmul2_rn(__fmul2_rn(__fmul2_rn(omt, omt), omt), sixth);
+    float2 a = __fmul2_rn(make_float2(3.f, 3.f), t3);
+    a = __fadd2_rn(a, __fmul2_rn(make_float2(-6.f, -6.f), t2));
+    w[1] = __fmul2_rn(__fadd2_rn(a, make_float2(4.f, 4.f)), sixth);
+    float2 b = __fmul2_rn(make_float2(-3.f, -3.f), t3);
+    b = __fadd2_rn(b, __fmul2_rn(make_float2(3.f, 3.f), t2));
+    b = __fadd2_rn(b, __fmul2_rn(make_float2(3.f, 3.f), t));
+    w[2] = __fmul2_rn(__fadd2_rn(b, make_float2(1.f, 1.f)), sixth);
+    w[3] = __fmul2_rn(t3, sixth);
+}
+
+template <int M>
+__device__ __forceinline__ void weights4f_x2(float2 t, float2 (&w)[4]) {
+    if (M == BSPLINE)
+        bspline4f_x2(t, w);
+    else
+        lagrange4f_x2(t, w);
+}
+
 // two cubic stencils with paired FMAs: the taps of point A and point B load
 // into the two halves of one register pair; lane-for-lane identical to
 // cubic_fixed
@@ -319,7 +343,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 template <int M, int NF, class Op>
 __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
-    static_assert(M == LINEAR || M == CUBIC, "k_slf: linear / cubic only");
+    static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
     extern __shared__ __align__(16) unsigned char sdyn[];
     // offset arithmetic on the shared array itself (not through uintptr_t) so
@@ -457,13 +481,13 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
                 cp_async_wait_all();
                 __syncthreads();
             }
-            if (M == CUBIC) {
+            if (M == CUBIC || M == BSPLINE) {
 #pragma unroll
                 for (int u = 0; u < SL_TI; u += 2) {
                     float2 w0[4], w1[4], w2[4];
-                    lagrange4f_x2(make_float2(fr0[u], fr0[u + 1]), w0);
-                    lagrange4f_x2(make_float2(fr1[u], fr1[u + 1]), w1);
-                    lagrange4f_x2(make_float2(fr2[u], fr2[u + 1]), w2);
+                    weights4f_x2<M>(make_float2(fr0[u], fr0[u + 1]), w0);
+                    weights4f_x2<M>(make_float2(fr1[u], fr1[u + 1]), w1);
+                    weights4f_x2<M>(make_float2(fr2[u], fr2[u + 1]), w2);
                     const float2 r = cubic_fixed_x2(sbox + off[u], sbox + off[u + 1], w0, w1, w2);
                     vals[u][f] = r.x;
                     vals[u + 1][f] = r.y;
@@ -540,13 +564,31 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
     FRG_CHECK_LAUNCH();
 }
 
-// Every SL launch: fp32 linear / cubic gathers of fp32 fields take the TMA
-// engine, everything else (f64 parity path, nearest, converting sources) the
-// generic staged engine of sl_tile.cuh.
+// B-spline prefilter (spectral.cu): out = coefficients of the periodic cubic
+// B-spline interpolant of in (one field of g, dtype)
+void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st);
+// stream-ordered per-thread scratch for prefiltered copies (slot per field)
+void* bspline_scratch(int slot, size_t bytes);
+
+// Every SL launch: fp32 linear / cubic / B-spline gathers of fp32 fields take
+// the TMA engine, everything else (f64 parity path, nearest, converting
+// sources) the generic staged engine of sl_tile.cuh.  BSPLINE first replaces
+// every gathered source by its prefiltered coefficients.
 template <typename T, int NF, class Op>
-void launch_sl(const Dims& g, int method, const Op& op, cudaStream_t st) {
+void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
+    Op op = op_in;
+    if (method == BSPLINE) {
+        using V = typename Op::V;
+        FRG_REQUIRE(g.h0 == 0, "B-spline transport needs the global prefilter (single-GPU grids)");
+        for (int f = 0; f < NF; ++f) {
+            V* c = (V*)bspline_scratch(f, sizeof(V) * (size_t)g.N);
+            bspline_prefilter(g, tcode(V(0)), op.field(f), c, st);
+            op.set_field(f, c);
+        }
+    }
     if constexpr (std::is_same<T, float>::value && std::is_same<typename Op::V, float>::value) {
         if (method == CUBIC) return launch_slf<CUBIC, NF, Op>(g, op, st);
+        if (method == BSPLINE) return launch_slf<BSPLINE, NF, Op>(g, op, st);
         if (method == LINEAR) return launch_slf<LINEAR, NF, Op>(g, op, st);
     }
     launch_sl_generic<T, NF, Op>(g, method, op, st);

@@ -200,8 +200,8 @@ __device__ __forceinline__ void op_done(const Op& op, int p, const T (&vals)[NF]
 
 template <int M>
 struct Halo {
-    static constexpr int lo = (M == CUBIC ? 1 : 0);
-    static constexpr int hi = (M == CUBIC ? 2 : (M == LINEAR ? 1 : 0));
+    static constexpr int lo = ((M == CUBIC || M == BSPLINE) ? 1 : 0);
+    static constexpr int hi = ((M == CUBIC || M == BSPLINE) ? 2 : (M == LINEAR ? 1 : 0));
 };
 
 __device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
@@ -223,9 +223,9 @@ __device__ __forceinline__ T box_interp(const T* __restrict__ box, int S1, int S
         return (T(1) - t0) * ((T(1) - t1) * c00 + t1 * c01) + t0 * ((T(1) - t1) * c10 + t1 * c11);
     } else {
         T w0[4], w1[4], w2[4];
-        lagrange4(t0, w0);
-        lagrange4(t1, w1);
-        lagrange4(t2, w2);
+        weights4<T, M>(t0, w0);
+        weights4<T, M>(t1, w1);
+        weights4<T, M>(t2, w2);
         const int sa = S1 * S2;
         const T* p0 = box + ((r0 * S1 + r1) * S2 + r2);
         T acc = T(0);
@@ -489,6 +489,7 @@ void launch_sl_generic(const Dims& g, int method, const Op& op, cudaStream_t st)
         case NEAREST: k_sl<T, NEAREST, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
         case LINEAR: k_sl<T, LINEAR, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
         case CUBIC: k_sl<T, CUBIC, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
+        case BSPLINE: k_sl<T, BSPLINE, NF, Op><<<sl_grid(g), vox_block(), 0, st>>>(g, op); break;
         default: throw Error(E_ARG, "unknown interpolation method");
     }
     FRG_CHECK_LAUNCH();

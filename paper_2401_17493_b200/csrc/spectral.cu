@@ -190,6 +190,16 @@ __device__ __forceinline__ double symbol_of(const Dims& g, const Bin& b, int kin
             return r.alpha * s;
         }
         case SK_LAPLACIAN: return -ksq;
+        case SK_BSPLINE_PREFILTER: {
+            // periodic cubic B-spline interpolation condition per axis: the
+            // samples are (c_{j-1} + 4 c_j + c_{j+1}) / 6 of the coefficients
+            double s = 1.0;
+            for (int a = 0; a < 3; ++a) {
+                const int n = g.axis_len(a);
+                if (n > 1) s *= (4.0 + 2.0 * cos(TWO_PI * b.m[a] / n)) / 6.0;
+            }
+            return 1.0 / s;
+        }
         case SK_LOWPASS:
         case SK_HIGHPASS: {
             // diffops.py:283-289 — keep |k_i| < n_i / 4 on every axis
@@ -888,6 +898,11 @@ void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a
         k_slab_combine<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, i1_off, n1_loc, (cufftComplex*)a,
                                                                      (const cufftComplex*)b, r, invN, a != b, project);
     FRG_CHECK_LAUNCH();
+}
+
+void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st) {
+    RegSpec r{1.0, 1, 1, 0, 1e-4};
+    spectral_apply(g, dtype, 1, in, out, SK_BSPLINE_PREFILTER, r, st);
 }
 
 }  // namespace frg

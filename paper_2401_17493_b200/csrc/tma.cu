@@ -38,13 +38,33 @@ void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
 void build_tile_plan(const Dims& g, int method, const float* disp, int4* plan, cudaStream_t st) {
     DispSrc<float> ds = disp_src(g, disp);
     ds.plan = nullptr;
-    if (method == CUBIC)
+    if (method == CUBIC || method == BSPLINE)  // same stencil geometry
         k_tile_plan<float, CUBIC><<<sl_grid(g), vox_block(), 0, st>>>(g, ds, plan);
     else if (method == LINEAR)
         k_tile_plan<float, LINEAR><<<sl_grid(g), vox_block(), 0, st>>>(g, ds, plan);
     else
         throw Error(E_ARG, "tile plans are built for linear / cubic maps");
     FRG_CHECK_LAUNCH();
+}
+
+namespace {
+struct Scratch {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+thread_local Scratch g_bs_scratch[16];
+}  // namespace
+
+void* bspline_scratch(int slot, size_t bytes) {
+    FRG_REQUIRE(slot >= 0 && slot < 16, "too many B-spline sources in one launch");
+    Scratch& s = g_bs_scratch[slot];
+    if (bytes > s.cap) {
+        if (s.p) FRG_CUDA(cudaFree(s.p));
+        s.p = nullptr;
+        FRG_CUDA(cudaMalloc(&s.p, bytes));
+        s.cap = bytes;
+    }
+    return s.p;
 }
 
 }  // namespace frg

@@ -43,6 +43,7 @@ static void sample_q_t(const V* vals, const Dims& g, const double* q0, const dou
         case NEAREST: k_sample_q<V, O, NEAREST><<<nb, TPB, 0, st>>>(vals, g, q0, q1, q2, npts, out); break;
         case LINEAR: k_sample_q<V, O, LINEAR><<<nb, TPB, 0, st>>>(vals, g, q0, q1, q2, npts, out); break;
         case CUBIC: k_sample_q<V, O, CUBIC><<<nb, TPB, 0, st>>>(vals, g, q0, q1, q2, npts, out); break;
+        case BSPLINE: k_sample_q<V, O, BSPLINE><<<nb, TPB, 0, st>>>(vals, g, q0, q1, q2, npts, out); break;
         default: throw Error(E_ARG, "unknown interpolation method");
     }
     FRG_CHECK_LAUNCH();
@@ -50,6 +51,13 @@ static void sample_q_t(const V* vals, const Dims& g, const double* q0, const dou
 
 void sample_q(const void* vals, int dtype, const Dims& g, const double* q0, const double* q1,
               const double* q2, long long npts, int method, void* out, cudaStream_t st) {
+    if (method == BSPLINE) {
+        // B-spline: sample the prefiltered coefficients (float grids only)
+        FRG_REQUIRE(dtype == F32 || dtype == F64, "bspline interpolation needs float values");
+        void* c = bspline_scratch(0, (size_t)g.N * (dtype == F64 ? 8 : 4));
+        bspline_prefilter(g, dtype, vals, c, st);
+        vals = c;
+    }
     if (dtype == F64)
         sample_q_t((const double*)vals, g, q0, q1, q2, npts, method, (double*)out, st);
     else if (dtype == F32)
@@ -74,6 +82,7 @@ struct DepartureOp {
     T sc[3];             // per component: h_t / h_axis
     T* out[3];           // per component
     int axis_of[3];
+    void set_field(int f, const VI* p) { v[f] = p; }
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const {
         T dd[3] = {T(0), T(0), T(0)};
 #pragma unroll
@@ -174,6 +183,7 @@ struct GatherOp {
     T* out[NF];
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int f) const { return in[f]; }
+    void set_field(int f, const T* p) { in[f] = p; }
     __device__ __forceinline__ void done(int p, const T (&vals)[NF]) const {
 #pragma unroll
         for (int f = 0; f < NF; ++f) out[f][p] = vals[f];
@@ -238,6 +248,7 @@ struct AdjMultOp {
     T ht;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int) const { return divv; }
+    void set_field(int, const T* p) { divv = p; }
     using Pre = T;
     __device__ __forceinline__ T pre(int p) const { return divl[p]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[1], T b) const {
@@ -255,6 +266,7 @@ struct AdjStepOp {
     T* out;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int) const { return u; }
+    void set_field(int, const T* p) { u = p; }
     using Pre = T;
     __device__ __forceinline__ T pre(int p) const { return cmul[p]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[1], T c) const { out[p] = vals[0] * c; }

@@ -120,6 +120,7 @@ struct ComposeOp {
     T* Dout[D];
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { cur.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int f) const { return step[f]; }
+    void set_field(int f, const T* p) { step[f] = p; }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
 #pragma unroll
         for (int c = 0; c < D; ++c) Dout[c][p] = Din[c][p] + vals[c];

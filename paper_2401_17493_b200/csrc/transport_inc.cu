@@ -31,6 +31,7 @@ struct IncFirstOp {
     T fsign, hh;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int f) const { return vtT[f]; }
+    void set_field(int f, const T* p) { vtT[f] = p; }
     // Tile epilogue (the TI voxels of one thread, p0 + u * pstride): the
     // gradient loads of all voxels for one j are independent read-only loads
     // in flight together, instead of one dependent round trip per voxel and j.
@@ -104,6 +105,7 @@ struct IncStepOp {
     T fsign;
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int) const { return mj; }
+    void set_field(int, const T* p) { mj = p; }
     using Pre = T;
     __device__ __forceinline__ T pre(int p) const { return Sj[p]; }
     __device__ __forceinline__ void done(int p, const T (&vals)[1], T s) const {
