@@ -305,7 +305,7 @@ def run_b200(a):
             "config": dict(config(n, a.precision), parallelism=f"independent 256^3 problem per rank x{world}"),
             "e2e": e2e, "gpu_launches": gpu_launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_gather<float,CUBIC> (one SL gather step)",
+                         "traffic": traffic, "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> (one TMA-staged SL gather step, frg_gather)",
                          "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather, "peak_source": peak_src},
             "matvec_roofline": matvec_roofline,
             "time_to_solution": tts,
