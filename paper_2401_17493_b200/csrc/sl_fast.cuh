@@ -37,7 +37,13 @@ namespace frg {
 // instruction), so the column origin is rounded down to a multiple of 4.
 // Row pitch 64 (= 0 mod 32 banks): lanes of a warp whose stencils sit on
 // different box rows still hit distinct banks (their columns differ).
-constexpr int TB_K = 64, TB_J = 16, TB_I = 12;
+#ifndef FRG_TB_J
+#define FRG_TB_J 16
+#endif
+#ifndef FRG_TB_I
+#define FRG_TB_I 12
+#endif
+constexpr int TB_K = 64, TB_J = FRG_TB_J, TB_I = FRG_TB_I;
 constexpr int TB_VOL = TB_K * TB_J * TB_I;
 constexpr int TB_PLANE = TB_K * TB_J;
 
@@ -367,10 +373,28 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     int4 pe = make_int4(0, 0, 0, 0);
     if (plan) pe = __ldg(plan + (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
 
+    // every independent global load first (displacements, epilogue inputs,
+    // plan entry), so the CTA pays one memory latency, not three in a row
+    bool ok[SL_TI];
+    float dsp[SL_TI][3];
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const int i = i_base + u;
+        ok[u] = in_kj && i < g.n0;
+        dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
+        if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, dsp[u][0], dsp[u][1], dsp[u][2]);
+    }
+    using PreT = typename PreOf<Op>::type;
+    PreT pre[SL_TI];
+    if constexpr (HasPre<Op>::value) {
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u)
+            if (ok[u]) pre[u] = op.pre(((i_base + u) * g.n1 + j) * g.n2 + k);
+    }
+
     int lo0, lo1, lo2, S0, S1, S2;
     if (plan) {
-        // precomputed box: issue the TMA first (the displacement loads below
-        // overlap its latency), no block reduction
+        // precomputed box: issue the TMA as soon as the plan entry arrives
         if (pe.w < 0) return;  // empty tile
         lo0 = pe.x;
         lo1 = pe.y;
@@ -384,14 +408,11 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     }
     int base0[SL_TI], base1[SL_TI], base2[SL_TI];
     float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
-    bool ok[SL_TI];
     int mn0 = INT_MAX, mn1 = INT_MAX, mn2 = INT_MAX, mx0 = INT_MIN, mx1 = INT_MIN, mx2 = INT_MIN;
 #pragma unroll
     for (int u = 0; u < SL_TI; ++u) {
         const int i = i_base + u;
-        ok[u] = in_kj && i < g.n0;
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f;
-        if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, d0, d1, d2);
+        const float d0 = dsp[u][0], d1 = dsp[u][1], d2 = dsp[u][2];
         const float f0 = floorf(d0), f1 = floorf(d1), f2 = floorf(d2);
         base0[u] = i + (int)f0;
         base1[u] = j + (int)f1;
@@ -444,14 +465,6 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     }
     const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
 
-    // epilogue inputs: loads in flight while the box lands and the stencils run
-    using PreT = typename PreOf<Op>::type;
-    PreT pre[SL_TI];
-    if constexpr (HasPre<Op>::value) {
-#pragma unroll
-        for (int u = 0; u < SL_TI; ++u)
-            if (ok[u]) pre[u] = op.pre(((i_base + u) * g.n1 + j) * g.n2 + k);
-    }
 
     float vals[SL_TI][NF];
     if (fits) {
