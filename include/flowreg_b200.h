@@ -107,6 +107,15 @@ int frg_points_to_disp(const int32_t n[3], int32_t d, int32_t dtype, const void*
 int frg_gather(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, const void* disp, int32_t nf,
                const void* const* in, void* const* out, void* stream);
 /* series[0] holds m0; fills series[1..n_t]                                   transport.py:83-98 */
+/* SL tile plan of an fp32 displacement map (one int4 per 32x8x4 tile: the
+ * stencil bounding box), built once per map and reused by every gather on it
+ * (frg_gather_planned); the KKT context builds and binds its own plans. */
+int64_t frg_tile_plan_count(const int32_t n[3]);
+int frg_tile_plan(const int32_t n[3], int32_t d, int32_t method, const void* disp, void* plan, void* stream);
+/* frg_gather for fp32 fields with a prebuilt plan of `disp` */
+int frg_gather_planned(const int32_t n[3], int32_t d, int32_t method, const void* disp, const void* plan, int32_t nf,
+                       const void* const* in, void* const* out, void* stream);
+
 int frg_solve_state(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, int32_t n_t, const void* disp,
                     void* series, void* stream);
 /* series[n_t] holds the final condition; fills series[0..n_t-1]             transport.py:105-135 */

@@ -56,6 +56,8 @@ PROTOTYPES = {
     "frg_disp_to_points": [_N3, _I, _I, _P, _P, _P],
     "frg_points_to_disp": [_N3, _I, _I, _P, _P, _P],
     "frg_gather": [_N3, _I, _I, _I, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _P],
+    "frg_tile_plan": [_N3, _I, _I, _P, _P, _P],
+    "frg_gather_planned": [_N3, _I, _I, _P, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _P],
     "frg_solve_state": [_N3, _I, _I, _I, _I, _P, _P, _P],
     "frg_solve_adjoint": [_N3, _I, _I, _I, _I, _P, _P, _P, _P],
     "frg_solve_inc_state": [_N3, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
@@ -128,6 +130,8 @@ def load(path: str = LIB_PATH):
             fn.restype = ctypes.c_int
         lib.frg_last_error.restype = ctypes.c_char_p
         lib.frg_last_error.argtypes = []
+        lib.frg_tile_plan_count.restype = ctypes.c_int64
+        lib.frg_tile_plan_count.argtypes = [_N3]
         lib.frg_version.restype = ctypes.c_char_p
         lib.frg_version.argtypes = []
         _lib = lib

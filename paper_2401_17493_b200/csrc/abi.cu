@@ -6,6 +6,7 @@
 
 #include "../../include/flowreg_b200.h"
 #include "kkt.h"
+#include "sl_fast.cuh"
 
 using namespace frg;
 
@@ -101,6 +102,32 @@ int frg_gather(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, con
         check_method(method);
         FRG_REQUIRE(nf >= 0, "nf must be >= 0");
         gather_fields(dims_of(n, d), dtype, method, disp, nf, in, out, ST(stream));
+    });
+}
+
+int64_t frg_tile_plan_count(const int32_t n[3]) {
+    try {
+        return (int64_t)tile_plan_count(dims_of(n, n[0] == 1 ? 2 : 3));
+    } catch (...) {
+        return -1;
+    }
+}
+
+int frg_tile_plan(const int32_t n[3], int32_t d, int32_t method, const void* disp, void* plan, void* stream) {
+    return guard([&] {
+        FRG_REQUIRE(method == FRG_LINEAR || method == FRG_CUBIC || method == FRG_BSPLINE,
+                    "tile plans are built for linear / cubic / bspline maps");
+        build_tile_plan(dims_of(n, d), method, (const float*)disp, (int4*)plan, ST(stream));
+    });
+}
+
+int frg_gather_planned(const int32_t n[3], int32_t d, int32_t method, const void* disp, const void* plan, int32_t nf,
+                       const void* const* in, void* const* out, void* stream) {
+    return guard([&] {
+        check_method(method);
+        FRG_REQUIRE(nf >= 0, "nf must be >= 0");
+        PlanScope ps(0, disp, (const int4*)plan, method);
+        gather_fields(dims_of(n, d), F32, method, disp, nf, in, out, ST(stream));
     });
 }
 

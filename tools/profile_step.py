@@ -41,6 +41,9 @@ f = torch.randn((n, n, n), generator=gen, dtype=torch.float32, device="cuda")
 g = torch.empty_like(f)
 ins = (ctypes.c_void_p * 1)(f.data_ptr())
 outs = (ctypes.c_void_p * 1)(g.data_ptr())
+plan = torch.empty((L.lib().frg_tile_plan_count(L.n3((n, n, n))), 4), dtype=torch.int32, device="cuda")
+L.check(L.lib().frg_tile_plan(L.n3((n, n, n)), 3, 2, ctypes.c_void_p(disp.data_ptr()), L.ptr(plan), L.stream()),
+        "tile_plan")
 
 
 def step():
@@ -51,8 +54,8 @@ def step():
     elif a.what == "refresh":
         st.refresh(v)
     else:
-        L.check(L.lib().frg_gather(L.n3((n, n, n)), 3, L.F32, 2, ctypes.c_void_p(disp.data_ptr()), 1, ins, outs,
-                                   L.stream()), "gather")
+        L.check(L.lib().frg_gather_planned(L.n3((n, n, n)), 3, 2, ctypes.c_void_p(disp.data_ptr()), L.ptr(plan), 1,
+                                           ins, outs, L.stream()), "gather")
 
 
 for _ in range(2):
