@@ -201,10 +201,60 @@ class KktState:
         return VectorField._wrap(self.grid, out)
 
     def hessian_matvec(self, vtilde: VectorField, out: torch.Tensor | None = None) -> VectorField:
-        """Gauss-Newton Hessian action; two PDE solves per call (kkt.py:237-260)."""
+        """Gauss-Newton Hessian action; two PDE solves per call (kkt.py:237-260).
+
+        ``vtilde`` may also be a HOST tensor (pinned, shape (d, *n)) with a
+        host ``out``: then the call is asynchronous and pipelined — the
+        host->device copy of call k+1 and the device->host copy of call k-1
+        overlap the device work of call k (two staging slots, dedicated copy
+        streams); ``out`` holds the result once the caller synchronises
+        (``torch.cuda.synchronize()`` or ``wait_host_io()``)."""
+        data = vtilde.data if hasattr(vtilde, "data") else vtilde
+        if isinstance(data, torch.Tensor) and data.device.type == "cpu":
+            return self._hessian_matvec_host(data, out)
         out = self._new() if out is None else out
         self._call("frg_kkt_hessian_matvec", L.ptr(self._vec(vtilde)), L.ptr(out))
         return VectorField._wrap(self.grid, out)
+
+    def _hessian_matvec_host(self, host_in: torch.Tensor, host_out: torch.Tensor | None) -> VectorField:
+        shape = (self.grid.d, *self.grid.n)
+        if tuple(host_in.shape) != shape or host_in.dtype != self.grid.torch_dtype:
+            raise ValueError(f"host v~ must be {shape} {self.grid.torch_dtype}")
+        if host_out is None:
+            host_out = torch.empty(shape, dtype=host_in.dtype).pin_memory()
+        io = getattr(self, "_io", None)
+        if io is None:
+            io = self._io = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(), "k": 0,
+                             "in": [self._new(), self._new()], "out": [self._new(), self._new()],
+                             "ev_in": [torch.cuda.Event(), torch.cuda.Event()],
+                             "ev_comp": [torch.cuda.Event(), torch.cuda.Event()],
+                             "ev_out": [torch.cuda.Event(), torch.cuda.Event()], "used": [False, False]}
+        s = io["k"] & 1
+        io["k"] += 1
+        cur = torch.cuda.current_stream()
+        self._call("frg_kkt_set_stream", ctypes.c_void_p(cur.cuda_stream))
+        with torch.cuda.stream(io["h2d"]):
+            if io["used"][s]:
+                io["h2d"].wait_event(io["ev_comp"][s])  # slot's previous matvec has consumed its input
+            io["in"][s].copy_(host_in, non_blocking=True)
+            io["ev_in"][s].record(io["h2d"])
+        cur.wait_event(io["ev_in"][s])
+        if io["used"][s]:
+            cur.wait_event(io["ev_out"][s])  # slot's previous result has left the device
+        self._call("frg_kkt_hessian_matvec", L.ptr(io["in"][s]), L.ptr(io["out"][s]))
+        io["ev_comp"][s].record(cur)
+        with torch.cuda.stream(io["d2h"]):
+            io["d2h"].wait_event(io["ev_comp"][s])
+            host_out.copy_(io["out"][s], non_blocking=True)
+            io["ev_out"][s].record(io["d2h"])
+        io["used"][s] = True
+        return VectorField._wrap(self.grid, host_out)
+
+    def wait_host_io(self) -> None:
+        """Make the current stream wait for every pending host-I/O matvec copy."""
+        io = getattr(self, "_io", None)
+        if io is not None:
+            torch.cuda.current_stream().wait_stream(io["d2h"])
 
     def mismatch(self) -> float:
         out = ctypes.c_double()
