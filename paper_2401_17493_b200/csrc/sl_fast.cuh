@@ -200,6 +200,11 @@ template <class Op>
 struct HasTile<Op, std::void_t<decltype(&Op::template done_tile<SL_TI>)>> : std::true_type {};
 
 template <class Op, class = void>
+struct HasTileSmem : std::false_type {};
+template <class Op>
+struct HasTileSmem<Op, std::void_t<decltype(&Op::template done_tile_smem<SL_TI>)>> : std::true_type {};
+
+template <class Op, class = void>
 struct PreOf {
     struct type {};
 };
@@ -529,6 +534,14 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
                 vals[u][f] = ok[u] ? global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u], base2[u],
                                                                     fr0[u], fr1[u], fr2[u])
                                    : 0.f;
+        }
+    }
+    if constexpr (HasTileSmem<Op>::value) {
+        if (fits && 12 * SL_TI * BX * BY <= TB_VOL) {
+            __syncthreads();  // the box is free once every thread is done with the last gather
+            op.template done_tile_smem<SL_TI>((i_base * g.n1 + j) * g.n2 + k, g.n1 * g.n2, ok, vals, sbox, tid,
+                                              BX * BY);
+            return;
         }
     }
     if constexpr (HasTile<Op>::value) {

@@ -72,6 +72,61 @@ struct IncFirstOp {
             }
         }
     }
+    // Shared-memory-staged tile epilogue (fp32, after the last gather, when
+    // the 48 KB box is free): the gradient slices of two time steps
+    // (grad m_j(y) and grad m_{j+1}, 12 fields x TI voxels per thread) are
+    // copied with cp.async all at once, so the epilogue pays ceil(n_t / 2)
+    // memory round trips with 48 loads in flight per thread instead of n_t
+    // round trips with 24.  Each thread reads back only what it copied: no
+    // CTA barrier between the stages.
+    template <int TI>
+    __device__ __forceinline__ void done_tile_smem(int p0, int pstride, const bool (&ok)[TI],
+                                                   const T (&vals)[TI][D], T* smem, int tid, int nthreads) const {
+        static_assert(sizeof(T) == 4, "smem-staged epilogue is the fp32 path");
+        T vx[TI][D];
+#pragma unroll
+        for (int u = 0; u < TI; ++u)
+#pragma unroll
+            for (int c = 0; c < D; ++c) vx[u][c] = ok[u] ? __ldg(vl[c] + p0 + u * pstride) : T(0);
+        auto slot = [&](int q, int u) -> T* { return smem + ((size_t)(q * TI + u) * nthreads + tid); };
+        for (int j0 = 0; j0 < n_t; j0 += 2) {
+            const int nj = (j0 + 1 < n_t) ? 2 : 1;
+            for (int jj = 0; jj < nj; ++jj) {
+                const int j = j0 + jj;
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+#pragma unroll
+                    for (int u = 0; u < TI; ++u)
+                        if (ok[u]) {
+                            const size_t p = (size_t)p0 + u * pstride;
+                            cp_async_elem<4>(slot(jj * 2 * D + c, u), gy + ((size_t)j * D + c) * N + p);
+                            cp_async_elem<4>(slot(jj * 2 * D + D + c, u), gx + ((size_t)(j + 1) * D + c) * N + p);
+                        }
+            }
+            cp_async_wait_all();
+            for (int jj = 0; jj < nj; ++jj) {
+                const int j = j0 + jj;
+#pragma unroll
+                for (int u = 0; u < TI; ++u) {
+                    if (!ok[u]) continue;
+                    T f0 = T(0), f1 = T(0);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        f0 -= *slot(jj * 2 * D + c, u) * vals[u][c];
+                        f1 -= *slot(jj * 2 * D + D + c, u) * vx[u][c];
+                    }
+                    const T sj = hh * (f0 + f1);
+                    const int p = p0 + u * pstride;
+                    if (j == 0) {
+                        if (m1) m1[p] = sj;
+                        if (fin) fin[p] = fsign * sj;
+                    } else {
+                        S[(size_t)(j - 1) * N + p] = sj;
+                    }
+                }
+            }
+        }
+    }
     __device__ __forceinline__ void done(int p, const T (&vals)[D]) const {
         T vx[D];
 #pragma unroll
