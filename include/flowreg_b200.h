@@ -167,6 +167,12 @@ int frg_kkt_create(const frg_config* cfg, void* stream, frg_kkt** out);
 int frg_kkt_destroy(frg_kkt* k);
 int frg_kkt_set_stream(frg_kkt* k, void* stream);
 /* images m0, m1 (N values, dtype) — copied into the context             kkt.py:139-162 */
+/* Interpolation precision of the SL steps of the GN Hessian matvec: 32
+ * (default; fp32 taps, 1e-5 parity) or 16 (north-star mixed-precision mode:
+ * the gathered incremental fields are rounded to fp16 taps, weights /
+ * accumulation / epilogues stay fp32; tolerance 1e-3 vs the f64 reference).
+ * State, adjoint, gradient and objective stay fp32.  Needs fp32 transport. */
+int frg_kkt_set_interp_precision(frg_kkt* k, int32_t bits);
 int frg_kkt_set_images(frg_kkt* k, const void* m0, const void* m1, int32_t dtype);
 /* all velocity-space vectors are control_dtype, d x N                      kkt.py:166-187 */
 int frg_kkt_refresh(frg_kkt* k, const void* v);

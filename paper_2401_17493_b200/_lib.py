@@ -83,6 +83,7 @@ PROTOTYPES = {
     "frg_kkt_destroy": [_P],
     "frg_kkt_set_stream": [_P, _P],
     "frg_kkt_set_images": [_P, _P, _P, _I],
+    "frg_kkt_set_interp_precision": [_P, _I],
     "frg_kkt_refresh": [_P, _P],
     "frg_kkt_objective": [_P, _DP],
     "frg_kkt_objective_at": [_P, _P, _DP],

@@ -371,6 +371,13 @@ int frg_kkt_set_stream(frg_kkt* k, void* stream) {
     });
 }
 
+int frg_kkt_set_interp_precision(frg_kkt* k, int32_t bits) {
+    return guard([&] {
+        CTX(k);
+        kkt_set_interp_bits(c, bits);
+    });
+}
+
 int frg_kkt_set_images(frg_kkt* k, const void* m0, const void* m1, int32_t dtype) {
     return guard([&] {
         CTX(k);

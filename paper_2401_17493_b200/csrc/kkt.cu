@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "kkt.h"
-#include "sl_fast.cuh"
+#include "sl_half.cuh"
 
 namespace frg {
 
@@ -51,6 +51,7 @@ struct KktCtx {
     DevBuf m0, m1, v, vT, negv, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
     DevBuf vtT, vty, mt, lt, bf, disp_trial, mtrial, gmC, tmp1, tmp2, tmp3;
     DevBuf plan_f, plan_b, plan_t;  // SL tile plans of disp_f / disp_b / disp_trial (fp32 maps)
+    int interp_bits = 32;           // 16: fp16-tap SL steps (mixed-precision interpolation mode)
     // two-level coarse pieces
     DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
     bool coarse_ready = false, h0_ready = false;
@@ -234,6 +235,12 @@ static void gradient_slices(KktCtx* k, int nslices, const void* u, void* out) {
     }
 }
 
+void kkt_set_interp_bits(KktCtx* k, int bits) {
+    FRG_REQUIRE(bits == 16 || bits == 32, "interpolation precision must be 16 or 32 bits");
+    FRG_REQUIRE(bits == 32 || k->tdt == F32, "fp16 interpolation needs fp32 transport");
+    k->interp_bits = bits;
+}
+
 void kkt_refresh(KktCtx* k, const void* v) {
     FRG_REQUIRE(k->have_images, "set_images must precede refresh");
     const long long N = k->N(), d = k->g.d;
@@ -375,6 +382,9 @@ void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
     const long long N = k->N();
     const size_t T = k->T();
     void* lt_final = k->lt.at<char>((size_t)k->n_t * N * T);
+    // fp16 taps act on the Gauss-Newton Hessian only (the inexact-Newton
+    // direction); state, adjoint, gradient and objective stay fp32
+    InterpScope is(k->interp_bits);
     PlanScope pf(0, k->disp_f.p, plan_of(k, k->plan_f), k->method);
     PlanScope pb(1, k->disp_b.p, plan_of(k, k->plan_b), k->method);
     if (k->distance == 0) {

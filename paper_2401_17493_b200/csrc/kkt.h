@@ -12,6 +12,8 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
                    cudaStream_t st);
 void kkt_destroy(KktCtx* k);
 void kkt_set_stream(KktCtx* k, cudaStream_t st);
+// 16: single-field SL steps with fp16 taps (mixed-precision interpolation); 32: fp32
+void kkt_set_interp_bits(KktCtx* k, int bits);
 void kkt_set_images(KktCtx* k, const void* m0, const void* m1, int dtype);
 void kkt_refresh(KktCtx* k, const void* v);
 double kkt_objective(KktCtx* k);

@@ -590,34 +590,4 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
     FRG_CHECK_LAUNCH();
 }
 
-// B-spline prefilter (spectral.cu): out = coefficients of the periodic cubic
-// B-spline interpolant of in (one field of g, dtype)
-void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st);
-// stream-ordered per-thread scratch for prefiltered copies (slot per field)
-void* bspline_scratch(int slot, size_t bytes);
-
-// Every SL launch: fp32 linear / cubic / B-spline gathers of fp32 fields take
-// the TMA engine, everything else (f64 parity path, nearest, converting
-// sources) the generic staged engine of sl_tile.cuh.  BSPLINE first replaces
-// every gathered source by its prefiltered coefficients.
-template <typename T, int NF, class Op>
-void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
-    Op op = op_in;
-    if (method == BSPLINE) {
-        using V = typename Op::V;
-        FRG_REQUIRE(g.h0 == 0, "B-spline transport needs the global prefilter (single-GPU grids)");
-        for (int f = 0; f < NF; ++f) {
-            V* c = (V*)bspline_scratch(f, sizeof(V) * (size_t)g.N);
-            bspline_prefilter(g, tcode(V(0)), op.field(f), c, st);
-            op.set_field(f, c);
-        }
-    }
-    if constexpr (std::is_same<T, float>::value && std::is_same<typename Op::V, float>::value) {
-        if (method == CUBIC) return launch_slf<CUBIC, NF, Op>(g, op, st);
-        if (method == BSPLINE) return launch_slf<BSPLINE, NF, Op>(g, op, st);
-        if (method == LINEAR) return launch_slf<LINEAR, NF, Op>(g, op, st);
-    }
-    launch_sl_generic<T, NF, Op>(g, method, op, st);
-}
-
 }  // namespace frg

@@ -1,0 +1,261 @@
+// fp16-tap SL gather engine: the north star's mixed-precision interpolation
+// path (tolerance 1e-3 vs the f64 reference).
+//
+// The gathered field is rounded to fp16 (one conversion pass per gather,
+// `to_half`), the TMA box holds fp16 (12 x 16 x 64 halves = 24 KB) and a copy
+// shifted by one element (another 24 KB) is built from it in shared memory,
+// so the four taps of every stencil row are TWO aligned 32-bit loads (half2
+// pairs (c, c+1), (c+2, c+3) from the copy matching the parity of c) instead
+// of four: 32 shared-memory loads per cubic point instead of 64, i.e. half of
+// the shared-memory bytes that bound the fp32 engine (sl_fast.cuh).  Weights,
+// accumulation, displacements and every epilogue stay fp32.  Single-field
+// steps with a tile plan (the state / adjoint / incremental SL steps); other
+// launches fall back to the fp32 engine.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "sl_fast.cuh"
+
+namespace frg {
+
+// host: 2D map over an fp16 field viewed as ((n0 + 2 h0) n1) rows x n2, box 16 x 64 halves
+void encode_field_map_half(CUtensorMap* map, const __half* ptr, const Dims& g);
+// host: fp32 -> fp16 copy of one source field (n0 + 2 h0 planes) into per-thread scratch
+const __half* half_copy(const Dims& g, const float* src, cudaStream_t st);
+// interpolation precision of the SL steps launched by this host thread (16 or 32)
+int& sl_interp_bits();
+
+// scope: SL steps launched by this host thread use `bits`-bit taps
+struct InterpScope {
+    int old;
+    explicit InterpScope(int bits) : old(sl_interp_bits()) { sl_interp_bits() = bits; }
+    ~InterpScope() { sl_interp_bits() = old; }
+};
+
+struct SlhSmem {
+    static constexpr size_t bytes = 2 * (size_t)TB_VOL * sizeof(__half) + 1024;
+};
+
+__device__ __forceinline__ float2 h2f(unsigned w) {
+    __half2 h = *reinterpret_cast<__half2*>(&w);
+    return __half22float2(h);
+}
+
+// one stencil row: taps (c, c+1, c+2, c+3) as two half2 words -> w . taps
+__device__ __forceinline__ float row_dot(const unsigned* __restrict__ rw, float2 w01, float2 w23) {
+    float2 acc = __fmul2_rn(w01, h2f(rw[0]));
+    acc = __ffma2_rn(w23, h2f(rw[1]), acc);
+    return acc.x + acc.y;
+}
+
+template <int M, class Op>
+__global__ void __launch_bounds__(BX* BY, 4)
+    k_slh(Dims g, Op op, const __grid_constant__ TmaMaps<1> maps, const __half* __restrict__ src16) {
+    static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slh: linear / cubic / B-spline");
+    extern __shared__ __align__(16) unsigned char sdyn[];
+    __half* b0 = reinterpret_cast<__half*>(sdyn + ((1024u - (smem_u32(sdyn) & 1023u)) & 1023u));
+    __half* b1 = b0 + TB_VOL;  // b1[x] = b0[x + 1]
+    __shared__ __align__(8) uint64_t bar;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+    const int k = blockIdx.x * BX + tx;
+    const int j = blockIdx.y * BY + ty;
+    const int i_base = blockIdx.z * SL_TI;
+    const bool in_kj = (k < g.n2) && (j < g.n1);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    const int4 pe = __ldg(op.ds.plan + (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    bool ok[SL_TI];
+    float dsp[SL_TI][3];
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const int i = i_base + u;
+        ok[u] = in_kj && i < g.n0;
+        dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
+        if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, dsp[u][0], dsp[u][1], dsp[u][2]);
+    }
+    using PreT = typename PreOf<Op>::type;
+    PreT pre[SL_TI];
+    if constexpr (HasPre<Op>::value) {
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u)
+            if (ok[u]) pre[u] = op.pre(((i_base + u) * g.n1 + j) * g.n2 + k);
+    }
+    if (pe.w < 0) return;  // empty tile
+    const int lo0 = pe.x, lo1 = pe.y, lo2 = pe.z & ~7;  // fp16 TMA box start: 16-byte aligned
+    const int S0 = pe.w & 1023, S1 = (pe.w >> 10) & 1023, S2 = ((pe.w >> 20) & 1023) + (pe.z - lo2);
+    const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
+    if (tid == 0 && fits) {
+        mbar_expect_tx(&bar, (unsigned)(S0 * TB_PLANE * sizeof(__half)));
+        for (int a = 0; a < S0; ++a)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3}], [%4];\n" ::"r"(smem_u32(b0 + a * TB_PLANE)),
+                "l"((unsigned long long)&maps.m[0]), "r"(lo2), "r"(src_plane(g, lo0 + a) * g.n1 + lo1),
+                "r"(smem_u32(&bar))
+                : "memory");
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+
+    int base0[SL_TI], base1[SL_TI], base2[SL_TI];
+    float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u) {
+        const float f0 = floorf(dsp[u][0]), f1 = floorf(dsp[u][1]), f2 = floorf(dsp[u][2]);
+        base0[u] = i_base + u + (int)f0;
+        base1[u] = j + (int)f1;
+        base2[u] = k + (int)f2;
+        fr0[u] = dsp[u][0] - f0;
+        fr1[u] = dsp[u][1] - f1;
+        fr2[u] = dsp[u][2] - f2;
+    }
+    float vals[SL_TI][1];
+    if (fits) {
+        mbar_wait_sleep(&bar, 0u);
+        if (lo1 < 0 || lo1 + S1 > g.n1 || lo2 < 0 || lo2 + S2 > g.n2) {
+            // rows / columns leaving the grid: copy from their periodic images
+            const int total = S0 * S1 * S2;
+            for (int e = tid; e < total; e += BX * BY) {
+                int r = e / S2;
+                const int c = e - r * S2;
+                const int a = r / S1;
+                const int b = r - a * S1;
+                if (lo1 + b >= 0 && lo1 + b < g.n1 && lo2 + c >= 0 && lo2 + c < g.n2) continue;
+                const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+                b0[(a * TB_J + b) * TB_K + c] = src16[((size_t)gi * g.n1 + gj) * g.n2 + gk];
+            }
+            __syncthreads();
+        }
+        // shifted copy: word w of b1 = (b0[2w + 1], b0[2w + 2])
+        {
+            const unsigned* w0 = reinterpret_cast<const unsigned*>(b0);
+            unsigned* w1 = reinterpret_cast<unsigned*>(b1);
+            const int words = S0 * TB_PLANE / 2;
+            for (int w = tid; w < words; w += BX * BY) w1[w] = __byte_perm(w0[w], w0[w + 1], 0x5432);
+        }
+        __syncthreads();
+        const unsigned* W0 = reinterpret_cast<const unsigned*>(b0);
+        const unsigned* W1 = reinterpret_cast<const unsigned*>(b1);
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u) {
+            float r = 0.f;
+            if (M == LINEAR) {
+                // taps (c, c + 1) of four rows from the parity-matched copy
+                const int o = ok[u] ? ((base0[u] - lo0) * TB_J + (base1[u] - lo1)) * TB_K + (base2[u] - lo2) : 0;
+                const unsigned* P = ((o & 1) ? W1 : W0) + (o >> 1);
+                const float t0 = fr0[u], t1 = fr1[u], t2 = fr2[u];
+                const float2 c00 = h2f(P[0]), c01 = h2f(P[TB_K / 2]), c10 = h2f(P[TB_PLANE / 2]),
+                             c11 = h2f(P[(TB_PLANE + TB_K) / 2]);
+                const float e00 = (1.f - t2) * c00.x + t2 * c00.y, e01 = (1.f - t2) * c01.x + t2 * c01.y;
+                const float e10 = (1.f - t2) * c10.x + t2 * c10.y, e11 = (1.f - t2) * c11.x + t2 * c11.y;
+                r = (1.f - t0) * ((1.f - t1) * e00 + t1 * e01) + t0 * ((1.f - t1) * e10 + t1 * e11);
+            } else {
+                const int o = ok[u] ? ((base0[u] - 1 - lo0) * TB_J + (base1[u] - 1 - lo1)) * TB_K + (base2[u] - 1 - lo2)
+                                    : 0;
+                const unsigned* P = ((o & 1) ? W1 : W0) + (o >> 1);
+                float w0[4], w1[4], w2[4];
+                if (M == BSPLINE) {
+                    bspline4(fr0[u], w0);
+                    bspline4(fr1[u], w1);
+                    bspline4(fr2[u], w2);
+                } else {
+                    lagrange4f(fr0[u], w0);
+                    lagrange4f(fr1[u], w1);
+                    lagrange4f(fr2[u], w2);
+                }
+                const float2 w01 = make_float2(w2[0], w2[1]), w23 = make_float2(w2[2], w2[3]);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    float plane = 0.f;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) plane = fmaf(w1[b], row_dot(P + (a * TB_PLANE + b * TB_K) / 2, w01, w23),
+                                                             plane);
+                    r = fmaf(w0[a], plane, r);
+                }
+            }
+            vals[u][0] = r;
+        }
+    } else {
+        // the box does not fit: fp32 gathers from global memory (rare)
+        Dims gsrc = g;
+        gsrc.n0 = g.n0 + 2 * g.h0;
+        const float* src = op.field(0);
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u)
+            vals[u][0] = ok[u] ? global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u], base2[u], fr0[u],
+                                                                fr1[u], fr2[u])
+                               : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < SL_TI; ++u)
+        if (ok[u]) {
+            const int p = ((i_base + u) * g.n1 + j) * g.n2 + k;
+            if constexpr (HasPre<Op>::value)
+                op.done(p, vals[u], pre[u]);
+            else
+                op.done(p, vals[u]);
+        }
+}
+
+// true when the fp16-tap engine ran this launch
+template <int M, class Op>
+bool launch_slh(const Dims& g, const Op& op, cudaStream_t st) {
+    if constexpr (HasDs<Op>::value) {
+        if (!op.ds.plan || plan_method(op.ds.plan) != M || !tma_grid_ok(g)) return false;
+        const __half* h = half_copy(g, op.field(0), st);
+        TmaMaps<1> maps;
+        encode_field_map_half(&maps.m[0], h, g);
+        static bool attr = false;
+        if (!attr) {
+            FRG_CUDA(cudaFuncSetAttribute(k_slh<M, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SlhSmem::bytes));
+            attr = true;
+        }
+        k_slh<M, Op><<<sl_grid(g), vox_block(), SlhSmem::bytes, st>>>(g, op, maps, h);
+        FRG_CHECK_LAUNCH();
+        return true;
+    }
+    return false;
+}
+
+// B-spline prefilter (spectral.cu): out = coefficients of the periodic cubic
+// B-spline interpolant of in (one field of g, dtype)
+void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st);
+// stream-ordered per-thread scratch for prefiltered copies (slot per field)
+void* bspline_scratch(int slot, size_t bytes);
+
+// Every SL launch: fp32 linear / cubic / B-spline gathers of fp32 fields take
+// the TMA engine (single-field steps the fp16-tap engine when the host thread
+// selected 16-bit interpolation and the map has a tile plan), everything else (f64 parity path, nearest, converting
+// sources) the generic staged engine of sl_tile.cuh.  BSPLINE first replaces
+// every gathered source by its prefiltered coefficients.
+template <typename T, int NF, class Op>
+void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
+    Op op = op_in;
+    if (method == BSPLINE) {
+        using V = typename Op::V;
+        FRG_REQUIRE(g.h0 == 0, "B-spline transport needs the global prefilter (single-GPU grids)");
+        for (int f = 0; f < NF; ++f) {
+            V* c = (V*)bspline_scratch(f, sizeof(V) * (size_t)g.N);
+            bspline_prefilter(g, tcode(V(0)), op.field(f), c, st);
+            op.set_field(f, c);
+        }
+    }
+    if constexpr (std::is_same<T, float>::value && std::is_same<typename Op::V, float>::value) {
+        if constexpr (NF == 1) {
+            if (sl_interp_bits() == 16) {
+                if (method == CUBIC && launch_slh<CUBIC, Op>(g, op, st)) return;
+                if (method == BSPLINE && launch_slh<BSPLINE, Op>(g, op, st)) return;
+                if (method == LINEAR && launch_slh<LINEAR, Op>(g, op, st)) return;
+            }
+        }
+        if (method == CUBIC) return launch_slf<CUBIC, NF, Op>(g, op, st);
+        if (method == BSPLINE) return launch_slf<BSPLINE, NF, Op>(g, op, st);
+        if (method == LINEAR) return launch_slf<LINEAR, NF, Op>(g, op, st);
+    }
+    launch_sl_generic<T, NF, Op>(g, method, op, st);
+}
+
+}  // namespace frg

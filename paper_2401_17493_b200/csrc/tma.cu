@@ -5,7 +5,7 @@
 
 #include <mutex>
 
-#include "sl_fast.cuh"
+#include "sl_half.cuh"
 
 namespace frg {
 
@@ -33,6 +33,55 @@ void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+void encode_field_map_half(CUtensorMap* map, const __half* ptr, const Dims& g) {
+    FRG_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA field must be 16-byte aligned");
+    FRG_REQUIRE(g.n2 % 8 == 0, "fp16 TMA rows must be multiples of 16 bytes");
+    const cuuint64_t dims[2] = {(cuuint64_t)g.n2, (cuuint64_t)(g.n0 + 2 * g.h0) * g.n1};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.n2 * 2};
+    const cuuint32_t box[2] = {TB_K, TB_J};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)ptr, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled (fp16) failed (" + std::to_string((int)r) + ")");
+}
+
+__global__ void k_to_half(const float4* __restrict__ s, __half2* __restrict__ d, long long n4) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n4) {
+        const float4 x = s[i];
+        d[2 * i] = __floats2half2_rn(x.x, x.y);
+        d[2 * i + 1] = __floats2half2_rn(x.z, x.w);
+    }
+}
+
+namespace {
+struct HalfScratch {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+thread_local HalfScratch g_half_scratch;
+thread_local int g_interp_bits = 32;
+}  // namespace
+
+int& sl_interp_bits() { return g_interp_bits; }
+
+const __half* half_copy(const Dims& g, const float* src, cudaStream_t st) {
+    const long long n = (long long)(g.n0 + 2 * g.h0) * g.n1 * g.n2;
+    FRG_REQUIRE(n % 4 == 0 && ((uintptr_t)src & 15) == 0, "fp16 copy needs 16-byte aligned fields");
+    HalfScratch& s = g_half_scratch;
+    const size_t bytes = (size_t)n * sizeof(__half);
+    if (bytes > s.cap) {
+        if (s.p) FRG_CUDA(cudaFree(s.p));
+        s.p = nullptr;
+        FRG_CUDA(cudaMalloc(&s.p, bytes));
+        s.cap = bytes;
+    }
+    k_to_half<<<blocks_for(n / 4, 256), 256, 0, st>>>((const float4*)src, (__half2*)s.p, n / 4);
+    FRG_CHECK_LAUNCH();
+    return (const __half*)s.p;
 }
 
 void build_tile_plan(const Dims& g, int method, const float* disp, int4* plan, cudaStream_t st) {

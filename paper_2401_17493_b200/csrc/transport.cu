@@ -9,7 +9,7 @@
 // Every SL time step is ONE launch of the shared-memory tiled gather engine
 // (sl_tile.cuh) with the step's pointwise update fused into its epilogue.
 #include "ops.h"
-#include "sl_fast.cuh"
+#include "sl_half.cuh"
 
 namespace frg {
 

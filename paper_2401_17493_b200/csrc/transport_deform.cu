@@ -1,6 +1,6 @@
 // Deformation tensor (transport.py:197-221) and composed map (transport.py:224-247).
 #include "ops.h"
-#include "sl_fast.cuh"
+#include "sl_half.cuh"
 
 namespace frg {
 

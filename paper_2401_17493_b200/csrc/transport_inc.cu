@@ -1,6 +1,6 @@
 // Incremental state transport (transport.py:147-176): fused SL step kernels.
 #include "ops.h"
-#include "sl_fast.cuh"
+#include "sl_half.cuh"
 
 #include <type_traits>
 

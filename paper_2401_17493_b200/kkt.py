@@ -65,7 +65,13 @@ class KktState:
 
     def __init__(self, m0: ScalarField, m1: ScalarField, reg: RegConfig, distance: str = "ssd",
                  method: str = "cubic", scheme: str = "fd8", v_init: VectorField | None = None,
-                 transport_dtype=None):
+                 transport_dtype=None, interp_precision: str = "fp32"):
+        """``interp_precision="fp16"`` selects the north star's mixed-precision
+        interpolation mode: the SL steps of the GN Hessian matvec gather fp16
+        taps (fp32 weights / accumulation; tolerance 1e-3), state / adjoint /
+        gradient stay fp32; needs fp32 transport."""
+        if interp_precision not in ("fp32", "fp16"):
+            raise ValueError(f"unknown interpolation precision {interp_precision!r}")
         if m0.grid != m1.grid:
             raise ValueError("images live on different grids")
         if distance not in L.DISTANCES:
@@ -95,6 +101,9 @@ class KktState:
         h = ctypes.c_void_p()
         L.check(L.lib().frg_kkt_create(ctypes.byref(cfg), L.stream(), ctypes.byref(h)), "kkt_create")
         self._h = h
+        self.interp_precision = interp_precision
+        if interp_precision == "fp16":
+            L.check(L.lib().frg_kkt_set_interp_precision(h, 16), "kkt_set_interp_precision")
         L.check(L.lib().frg_kkt_set_images(h, L.ptr(m0.values), L.ptr(m1.values), cdt), "kkt_set_images")
         self.refresh(v_init if v_init is not None else VectorField.zeros(grid))
 
