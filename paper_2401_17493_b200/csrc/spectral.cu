@@ -473,6 +473,9 @@ void spectral_apply(const Dims& g, int dtype, int ncomp, const void* in, void* o
     spectral_apply_ex(g_plans, ws, g, dtype, ncomp, in, out, kind, r, st);
 }
 
+void slab_combine_flat(const Dims& g, void* a, const void* b, const RegSpec& r, bool have_a, bool project, bool f64,
+                       cudaStream_t st);
+
 template <typename RA, typename RB>
 static void combine_t(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const RA* a, const RB* b, RA* out,
                       const RegSpec& r, bool project_on, cudaStream_t st) {
@@ -483,6 +486,14 @@ static void combine_t(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, cons
     CB* sb = (CB*)ws_b;
     if (a) fwd<RA>(pc, g, g.d, a, sa, st);
     fwd<RB>(pc, g, g.d, b, sb, st);
+    if constexpr (std::is_same<CA, CB>::value) {
+        // flat grid-stride combine (no idle lanes on the n2/2+1 rows)
+        if (g.n0 > 1 && g.d == 3) {
+            slab_combine_flat(g, (void*)sa, (const void*)sb, r, a != nullptr, project_on, sizeof(RA) == 8, st);
+            inv<RA>(pc, g, g.d, sa, out, st);
+            return;
+        }
+    }
     k_spec_combine<CA, CB><<<spec_grid(g), vox_block(), 0, st>>>(g, nh, sa, sb, r, 1.0 / (double)g.N, a != nullptr,
                                                                      project_on);
     FRG_CHECK_LAUNCH();
@@ -903,6 +914,20 @@ void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a
 void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st) {
     RegSpec r{1.0, 1, 1, 0, 1e-4};
     spectral_apply(g, dtype, 1, in, out, SK_BSPLINE_PREFILTER, r, st);
+}
+
+// whole-grid combine through the flat split-spectrum kernel (i1 offset 0, all rows)
+void slab_combine_flat(const Dims& g, void* a, const void* b, const RegSpec& r, bool have_a, bool project, bool f64,
+                       cudaStream_t st) {
+    const long long cnt = (long long)g.n0 * g.n1 * (g.n2 / 2 + 1);
+    const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
+    if (f64)
+        k_slab_combine<cufftDoubleComplex><<<slab_blocks(cnt), 256, 0, st>>>(
+            g, 0, g.n1, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, r, invN, have_a, project);
+    else
+        k_slab_combine<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, 0, g.n1, (cufftComplex*)a,
+                                                                     (const cufftComplex*)b, r, invN, have_a, project);
+    FRG_CHECK_LAUNCH();
 }
 
 }  // namespace frg

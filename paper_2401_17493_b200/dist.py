@@ -88,6 +88,8 @@ class SlabComm:
         if self.size == 1:
             out.copy_(inp)
             return
+        if out.is_complex():  # NCCL has no complex type: move the (re, im) pairs as reals
+            out, inp = torch.view_as_real(out), torch.view_as_real(inp)
         if self.staged:
             o = torch.empty(out.shape, dtype=out.dtype)
             tdist.all_to_all_single(o, inp.cpu(), group=self.group)
