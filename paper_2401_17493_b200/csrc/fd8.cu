@@ -64,7 +64,120 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_div(Dims g, const T* __restrict
     out[v.p] = acc;
 }
 
+// 2.5D-blocked gradient for single-GPU 3D grids: a CTA owns a 32 (k) x 8 (j)
+// column block of one slice and marches along axis 0 through FD8_CHUNK
+// planes.  The axis-0 derivative comes from a 9-value register window of
+// the thread's own column, the in-plane derivatives from a shared-memory
+// tile of the current plane with a 4-wide halo: ~3.5 loads per voxel instead
+// of 25 (mostly L2 re-reads of neighbouring planes).  Same per-term order as
+// fd8_line, so results are identical.
+constexpr int FD8_CHUNK = 16;
+
+template <typename T>
+__device__ __forceinline__ T fd8_taps(const T (&up)[5], const T (&um)[5], T inv840h) {
+    const T w[4] = {T(3), T(-32), T(168), T(-672)};  // s = 4, 3, 2, 1
+    T acc = T(0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int sh = 4 - q;
+        acc += w[q] * up[sh];
+        acc -= w[q] * um[sh];
+    }
+    return acc * inv840h;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BX * BY) k_fd8_grad_col(Dims g, int nslices, int nchunk, const T* __restrict__ u,
+                                                         T* __restrict__ out) {
+    __shared__ T tile[BY + 8][BX + 8];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+    const int k = blockIdx.x * BX + tx, j = blockIdx.y * BY + ty;
+    const int slice = blockIdx.z / nchunk, ch = blockIdx.z - slice * nchunk;
+    const int ib = ch * FD8_CHUNK, ie = min(ib + FD8_CHUNK, g.n0);
+    const T* __restrict__ us = u + (size_t)slice * g.N;
+    T* __restrict__ os = out + (size_t)slice * 3 * g.N;
+    const bool in = k < g.n2 && j < g.n1;
+    const long long plane = (long long)g.n1 * g.n2;
+    const T inv0 = T(1) / (T(840) * T(TWO_PI / g.n0)), inv1 = T(1) / (T(840) * T(TWO_PI / g.n1)),
+            inv2 = T(1) / (T(840) * T(TWO_PI / g.n2));
+    auto col = [&](int i) -> T {
+        int ii = i % g.n0;
+        if (ii < 0) ii += g.n0;
+        return in ? __ldg(us + ii * plane + (long long)j * g.n2 + k) : T(0);
+    };
+    T win[9];  // win[q] = u(i - 4 + q) of this column
+#pragma unroll
+    for (int q = 0; q < 8; ++q) win[q] = col(ib - 4 + q);
+    const int kb = blockIdx.x * BX - 4, jb = blockIdx.y * BY - 4;
+    // tile element e = tid + 256 q (q < 3) of the plane being prefetched
+    constexpr int TW = BX + 8, TE = (BY + 8) * (BX + 8);
+    int toff[3];
+    bool tin[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * BX * BY;
+        tin[q] = e < TE;
+        const int r = e / TW, c = e - r * TW;
+        int jj = jb + r, kk = kb + c;
+        jj = jj < 0 ? jj + g.n1 : (jj >= g.n1 ? jj - g.n1 : jj);
+        kk = kk < 0 ? kk + g.n2 : (kk >= g.n2 ? kk - g.n2 : kk);
+        toff[q] = tin[q] ? jj * g.n2 + kk : 0;
+    }
+    T nxt[3];
+    T wnext = col(ib + 4);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) nxt[q] = tin[q] ? __ldg(us + ib * plane + toff[q]) : T(0);
+    T* flat = &tile[0][0];
+    for (int i = ib; i < ie; ++i) {
+        __syncthreads();  // previous plane's tile fully consumed
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            if (tin[q]) flat[tid + q * BX * BY] = nxt[q];
+        win[8] = wnext;
+        __syncthreads();
+        if (i + 1 < ie) {  // next plane in flight while this one is differentiated
+            wnext = col(i + 5);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) nxt[q] = tin[q] ? __ldg(us + (i + 1) * plane + toff[q]) : T(0);
+        }
+        if (in) {
+            T up[5], um[5];
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = win[4 + sh];
+                um[sh] = win[4 - sh];
+            }
+            const size_t p = (size_t)i * plane + (size_t)j * g.n2 + k;
+            os[p] = fd8_taps<T>(up, um, inv0);
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = tile[ty + 4 + sh][tx + 4];
+                um[sh] = tile[ty + 4 - sh][tx + 4];
+            }
+            os[g.N + p] = fd8_taps<T>(up, um, inv1);
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = tile[ty + 4][tx + 4 + sh];
+                um[sh] = tile[ty + 4][tx + 4 - sh];
+            }
+            os[2 * g.N + p] = fd8_taps<T>(up, um, inv2);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) win[q] = win[q + 1];
+    }
+}
+
 void fd8_gradient(const Dims& g, int tdtype, int nslices, const void* u, void* out, cudaStream_t st) {
+    if (g.d == 3 && g.h0 == 0 && g.n0 >= 9 && g.n1 >= 9 && g.n2 >= 9) {
+        const int nchunk = (g.n0 + FD8_CHUNK - 1) / FD8_CHUNK;
+        dim3 grid((g.n2 + BX - 1) / BX, (g.n1 + BY - 1) / BY, nslices * nchunk);
+        if (tdtype == F64)
+            k_fd8_grad_col<double><<<grid, vox_block(), 0, st>>>(g, nslices, nchunk, (const double*)u, (double*)out);
+        else
+            k_fd8_grad_col<float><<<grid, vox_block(), 0, st>>>(g, nslices, nchunk, (const float*)u, (float*)out);
+        FRG_CHECK_LAUNCH();
+        return;
+    }
     FRG_REQUIRE(g.h0 == 0 || g.h0 >= 4, "slab FD8 needs >= 4 ghost planes");
     for (int c = 0; c < g.d; ++c)
         FRG_REQUIRE(g.axis_glob(g.comp_axis(c)) >= 9, "8th-order stencil needs n_i >= 9");
