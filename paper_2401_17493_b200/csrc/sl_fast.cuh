@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (tid < 6) bb[tid] = INT_MAX;
+    __syncthreads();  // barrier + bb initialised before anyone uses them (nothing is in flight yet)
 
     const int4* plan = nullptr;
     if constexpr (HasDs<Op>::value) plan = op.ds.plan;
@@ -409,7 +410,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
         S2 = (pe.w >> 20) & 1023;
         if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
             tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
-        __syncthreads();  // barrier initialised before anyone waits on it
+        // no CTA barrier here: the other warps go on with their displacement
+        // arithmetic while thread 0 waits for the plan entry and issues the TMA
     }
     int base0[SL_TI], base1[SL_TI], base2[SL_TI];
     float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
@@ -442,7 +444,6 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     mx0 = warp_max_i(mx0);
     mx1 = warp_max_i(mx1);
     mx2 = warp_max_i(mx2);
-    __syncthreads();  // bb initialised
     if (tx == 0 && mn0 != INT_MAX) {
         atomicMin(&bb[0], mn0);
         atomicMin(&bb[1], mn1);
