@@ -202,9 +202,11 @@ def run_b200(a):
     ms_per_step = t_ms / a.steps
     value = world * a.steps / (t_ms / 1e3)
 
-    # launches of OUR kernels per matvec (from the host call sequence in csrc/kkt.cu:
-    # inc-state 4, adjoint 4, body force 1, combine 1) plus cuFFT transforms (9)
-    launches_per_matvec = 4 + 4 + 1 + 1
+    # launches of OUR kernels per matvec (host call sequence of kkt_hessian_matvec,
+    # profiles/r01_launches_matvec_final_summary.txt): v~ f64->f32 convert 1,
+    # inc-state 4 (IncFirst + 3 IncStep), adjoint 4, body force 1, spectral
+    # combine 1, f32->f64 output convert 1 (+ 9 cuFFT transforms, not counted)
+    launches_per_matvec = 1 + 4 + 4 + 1 + 1 + 1
     gpu_launches = launches_per_matvec * a.steps
 
     # --- dominant kernel roofline: one cubic SL gather step (k_gather) -------

@@ -30,9 +30,6 @@ namespace frg {
 #define SL_TI_OVERRIDE 4
 #endif
 constexpr int SL_TI = SL_TI_OVERRIDE;  // voxels per thread along axis 0
-#ifndef FRG_SL_PAIRED
-#define FRG_SL_PAIRED 0
-#endif
 
 // box budget per CTA: 24 KB for fp32 (several CTAs per SM), 44 KB for the
 // f64 parity path (static shared memory is limited to 48 KB)
@@ -60,56 +57,6 @@ __device__ __forceinline__ unsigned fast_div(unsigned e, unsigned m) { return __
 __host__ __device__ __forceinline__ unsigned div_magic(unsigned d) {
     // floor((2^32 - 1) / d) + 1: exact floor(e / d) for e, d < 2^16 (32-bit division only)
     return 0xFFFFFFFFu / d + 1u;
-}
-
-// Two cubic stencils evaluated together with the Blackwell paired fp32 FMA
-// (FFMA2: __ffma2_rn / __fmul2_rn), halving the FP instruction count; the taps
-// are still scalar shared-memory loads.  Lane .x = point A, .y = point B.
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-
-__device__ __forceinline__ void lagrange4_x2(float2 t, float2 w[4]) {
-    const float2 one = f2(1.f, 1.f), two = f2(2.f, 2.f);
-    const float2 tm1 = __fadd2_rn(t, f2(-1.f, -1.f)), tm2 = __fadd2_rn(t, f2(-2.f, -2.f)),
-                 tp1 = __fadd2_rn(t, one);
-    const float2 sixth = f2(1.f / 6.f, 1.f / 6.f), half = f2(0.5f, 0.5f);
-    const float2 mt = f2(-t.x, -t.y), mtp1 = f2(-tp1.x, -tp1.y);
-    w[0] = __fmul2_rn(__fmul2_rn(__fmul2_rn(mt, tm1), tm2), sixth);
-    w[1] = __fmul2_rn(__fmul2_rn(__fmul2_rn(tp1, tm1), tm2), half);
-    w[2] = __fmul2_rn(__fmul2_rn(__fmul2_rn(mtp1, t), tm2), half);
-    w[3] = __fmul2_rn(__fmul2_rn(__fmul2_rn(tp1, t), tm1), sixth);
-    (void)two;
-}
-
-__device__ __forceinline__ float2 box_cubic_x2(const float* __restrict__ box, int S1, int S2, int oA, int oB,
-                                               float2 t0, float2 t1, float2 t2) {
-    float2 w0[4], w1[4], w2[4];
-    lagrange4_x2(t0, w0);
-    lagrange4_x2(t1, w1);
-    lagrange4_x2(t2, w2);
-    const int sa = S1 * S2;
-    const float* pA = box + oA;
-    const float* pB = box + oB;
-    float2 acc = f2(0.f, 0.f);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const float* rA = pA;
-        const float* rB = pB;
-        float2 plane = f2(0.f, 0.f);
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-            float2 r = __fmul2_rn(w2[0], f2(rA[0], rB[0]));
-            r = __ffma2_rn(w2[1], f2(rA[1], rB[1]), r);
-            r = __ffma2_rn(w2[2], f2(rA[2], rB[2]), r);
-            r = __ffma2_rn(w2[3], f2(rA[3], rB[3]), r);
-            plane = __ffma2_rn(w1[bb], r, plane);
-            rA += S2;
-            rB += S2;
-        }
-        acc = __ffma2_rn(w0[a], plane, acc);
-        pA += sa;
-        pB += sa;
-    }
-    return acc;
 }
 
 // The box is flattened over all CTA threads (e = tid + 256 r), row / column
@@ -373,33 +320,13 @@ __global__ void __launch_bounds__(BX * BY, (sizeof(T) == 4 && NF == 1) ? 4 : 2) 
             else
                 stage_box<T, typename Op::V>(box, src, g, lo0, lo1, lo2, S1, S2, S2p, (int)vol, tid);
             __syncthreads();
-            if constexpr (FRG_SL_PAIRED && M == CUBIC && sizeof(T) == 4 && SL_TI % 2 == 0) {
-                // paired FFMA2 evaluation; an inactive partner reuses its twin's taps
 #pragma unroll
-                for (int u = 0; u < SL_TI; u += 2) {
-                    const bool va = in_kj && i_base + u < g.n0, vb = in_kj && i_base + u + 1 < g.n0;
-                    if (!va) {
-                        vals[u][f] = vals[u + 1][f] = T(0);
-                        continue;
-                    }
-                    const int ub = vb ? u + 1 : u;
-                    const int oA = ((base0[u] - 1 - lo0) * S1 + (base1[u] - 1 - lo1)) * S2p + (base2[u] - 1 - lo2);
-                    const int oB =
-                        ((base0[ub] - 1 - lo0) * S1 + (base1[ub] - 1 - lo1)) * S2p + (base2[ub] - 1 - lo2);
-                    float2 r = box_cubic_x2((const float*)box, S1, S2p, oA, oB, f2(fr0[u], fr0[ub]),
-                                            f2(fr1[u], fr1[ub]), f2(fr2[u], fr2[ub]));
-                    vals[u][f] = r.x;
-                    vals[u + 1][f] = vb ? r.y : T(0);
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < SL_TI; ++u)
-                    vals[u][f] = (in_kj && i_base + u < g.n0)
-                                     ? box_interp<T, M>(box, S1, S2p, base0[u] - Halo<M>::lo - lo0,
-                                                        base1[u] - Halo<M>::lo - lo1, base2[u] - Halo<M>::lo - lo2,
-                                                        fr0[u], fr1[u], fr2[u])
-                                     : T(0);
-            }
+            for (int u = 0; u < SL_TI; ++u)
+                vals[u][f] = (in_kj && i_base + u < g.n0)
+                                 ? box_interp<T, M>(box, S1, S2p, base0[u] - Halo<M>::lo - lo0,
+                                                    base1[u] - Halo<M>::lo - lo1, base2[u] - Halo<M>::lo - lo2,
+                                                    fr0[u], fr1[u], fr2[u])
+                                 : T(0);
         }
     } else {
 #pragma unroll
