@@ -185,9 +185,14 @@ __device__ __forceinline__ void stage_fixed(float* __restrict__ box, const float
     }
 }
 
+#ifndef FRG_SL_DB
+#define FRG_SL_DB 0  // measured: 2 CTAs/SM with two 48 KB boxes lose more than the overlap gains
+#endif
 template <int NF>
 struct SlfSmem {
-    static constexpr int NB = 1;  // one 48 KB box per CTA (4 CTAs / SM)
+    // one 48 KB box per CTA for single-field steps (4 CTAs / SM); multi-field
+    // gathers double-buffer (the next field's TMA overlaps this field's taps)
+    static constexpr int NB = (NF > 1 && FRG_SL_DB) ? 2 : 1;
     // + 1 KB: the dynamic window is re-aligned to 1024 B in the kernel (the
     // compiler-placed start after the static shared variables is not)
     static constexpr size_t bytes = (size_t)NB * TB_VOL * sizeof(float) + 1024;
@@ -352,7 +357,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 }
 
 template <int M, int NF, class Op>
-__global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
+__global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : (SlfSmem<NF>::NB == 2 ? 2 : 3))
     k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
@@ -360,7 +365,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     // offset arithmetic on the shared array itself (not through uintptr_t) so
     // that the taps compile to LDS, not generic LD
     float* sbox = reinterpret_cast<float*>(sdyn + ((1024u - (smem_u32(sdyn) & 1023u)) & 1023u));
-    __shared__ __align__(8) uint64_t bar;
+    constexpr int NB = SlfSmem<NF>::NB;
+    __shared__ __align__(8) uint64_t bars[NB];
     __shared__ int bb[6];  // min0, min1, min2, -max0, -max1, -max2 of the stencil bases
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
     const int k = blockIdx.x * BX + tx;
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     const int i_base = blockIdx.z * SL_TI;
     const bool in_kj = (k < g.n2) && (j < g.n1);
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        for (int b = 0; b < NB; ++b) mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (tid < 6) bb[tid] = INT_MAX;
@@ -409,7 +415,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
         S1 = (pe.w >> 10) & 1023;
         S2 = (pe.w >> 20) & 1023;
         if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
-            tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
+            for (int b = 0; b < NB; ++b) tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
         // no CTA barrier here: the other warps go on with their displacement
         // arithmetic while thread 0 waits for the plan entry and issues the TMA
     }
@@ -467,7 +473,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
     S1 = mx1 + Halo<M>::hi - lo1 + 1;
     S2 = mx2 + Halo<M>::hi - lo2 + 1;
     if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
-        tma_box(sbox, &maps.m[0], g, lo0, lo1, lo2, S0, &bar);
+        for (int b = 0; b < NB; ++b) tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
     }
     const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
 
@@ -486,17 +492,18 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const float* src = op.field(f);
+            float* box = sbox + (f % NB) * TB_VOL;
             if (use_tma) {
-                mbar_wait_sleep(&bar, (unsigned)(f & 1));
+                mbar_wait_sleep(&bars[f % NB], (unsigned)((f / NB) & 1));
                 if (wrap) {  // planes already wrapped by tma_box
-                    patch_axis(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
-                    patch_axis(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
+                    patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
+                    patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
                     cp_async_wait_all();
                     __syncthreads();
                 }
             } else {
                 if (f > 0) __syncthreads();
-                stage_fixed(sbox, src, g, lo0, lo1, lo2, S0, S1, S2, tid);
+                stage_fixed(box, src, g, lo0, lo1, lo2, S0, S1, S2, tid);
                 cp_async_wait_all();
                 __syncthreads();
             }
@@ -507,19 +514,19 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? 4 : 3)
                     weights4f_x2<M>(make_float2(fr0[u], fr0[u + 1]), w0);
                     weights4f_x2<M>(make_float2(fr1[u], fr1[u + 1]), w1);
                     weights4f_x2<M>(make_float2(fr2[u], fr2[u + 1]), w2);
-                    const float2 r = cubic_fixed_x2(sbox + off[u], sbox + off[u + 1], w0, w1, w2);
+                    const float2 r = cubic_fixed_x2(box + off[u], box + off[u + 1], w0, w1, w2);
                     vals[u][f] = r.x;
                     vals[u + 1][f] = r.y;
                 }
             } else {
 #pragma unroll
-                for (int u = 0; u < SL_TI; ++u) vals[u][f] = linear_fixed(sbox + off[u], fr0[u], fr1[u], fr2[u]);
+                for (int u = 0; u < SL_TI; ++u) vals[u][f] = linear_fixed(box + off[u], fr0[u], fr1[u], fr2[u]);
             }
-            if (use_tma && f + 1 < NF) {
-                __syncthreads();  // every thread is done reading the box
+            if (use_tma && f + NB < NF) {
+                __syncthreads();  // every thread is done reading this buffer
                 if (tid == 0) {
                     fence_proxy_async();
-                    tma_box(sbox, &maps.m[f + 1], g, lo0, lo1, lo2, S0, &bar);
+                    tma_box(box, &maps.m[f + NB], g, lo0, lo1, lo2, S0, &bars[f % NB]);
                 }
             }
         }
