@@ -245,6 +245,16 @@ int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc,
 int frg_slab_spec_combine(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, void* a,
                           const void* b, const frg_reg* reg, int32_t project, void* stream);
 
+/* Bind a displacement map to its tile plan (frg_tile_plan) for the SL calls
+ * this host thread makes until frg_clear_plans (two slots: forward / backward
+ * map); used by the slab path, whose per-step calls carry only the map. */
+int frg_bind_plan(int32_t slot, const void* disp, const void* plan, int32_t method);
+int frg_clear_plans(void);
+/* trapezoid body force with a lambda slice stride (elements; slab series
+ * padded with ghost planes between slices) */
+int frg_slab_body_force(const int32_t n_loc[3], int32_t n_t, const void* lam, int64_t lam_stride, const void* grads,
+                        void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,6 +97,9 @@ PROTOTYPES = {
     "frg_kkt_set_counters": [_P, ctypes.POINTER(_L)],
     "frg_kkt_get": [_P, _I, _P],
     "frg_kkt_detgrad": [_P, _DP],
+    "frg_bind_plan": [_I, _P, _P, _I],
+    "frg_clear_plans": [],
+    "frg_slab_body_force": [_N3, _I, _P, _L, _P, _P, _P],
     # slab decomposition (multi-GPU, dist.py)
     "frg_slab_departure": [_N3, _I, _I, _I, _D, _P, _P, _P, _P],
     "frg_slab_gather": [_N3, _I, _I, _I, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _P],

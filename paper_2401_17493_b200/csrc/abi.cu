@@ -619,3 +619,31 @@ int frg_slab_spec_combine(const int32_t n_glob[3], int32_t i1_off, int32_t n1_lo
 
 }  // extern "C"
 
+extern "C" {
+
+// thread-local binding of a displacement map to its tile plan for the SL calls
+// this host thread makes afterwards (slab path: the C-ABI gathers receive the
+// map pointer only)
+int frg_bind_plan(int32_t slot, const void* disp, const void* plan, int32_t method) {
+    return guard([&] {
+        FRG_REQUIRE(slot == 0 || slot == 1, "plan slot must be 0 or 1");
+        g_plan_bind[slot].disp = disp;
+        g_plan_bind[slot].plan = (const int4*)plan;
+        g_plan_bind[slot].method = method;
+    });
+}
+
+int frg_clear_plans(void) {
+    return guard([&] { g_plan_bind[0] = g_plan_bind[1] = PlanBinding(); });
+}
+
+int frg_slab_body_force(const int32_t n_loc[3], int32_t n_t, const void* lam, int64_t lam_stride, const void* grads,
+                        void* out, void* stream) {
+    return guard([&] {
+        FRG_REQUIRE(n_t >= 1, "time integral needs at least 2 slices");
+        body_force(make_dims(n_loc, 3), F32, F32, n_t, lam, grads, out, false, ST(stream), lam_stride);
+    });
+}
+
+}  // extern "C"
+

@@ -55,7 +55,7 @@ void inc_state(const Dims& g, int tdtype, int cdtype, int method, int n_t, const
 // trapezoid body force b = sum_j w_j lam_j grad_j, written in odtype; if
 // accumulate, out += b
 void body_force(const Dims& g, int tdtype, int odtype, int n_t, const void* lam, const void* grads,
-                void* out, bool accumulate, cudaStream_t st);
+                void* out, bool accumulate, cudaStream_t st, long long lam_stride = 0);
 // deformation tensor endpoint F(1) (d*d x N, tdtype) and jacobian at x
 void deformation_tensor(const Dims& g, int tdtype, int method, int n_t, const void* disp,
                         const void* jac, void* F, void* work, cudaStream_t st);

@@ -356,13 +356,13 @@ __global__ void __launch_bounds__(TPB) k_body_force(Dims g, int n_t, const T* __
 // (5 lambda slices + 15 gradient fields in, 3 components out per voxel), same
 // per-voxel expression order as k_body_force
 __global__ void __launch_bounds__(TPB) k_body_force_f4(long long N4, int n_t, int d, const float4* __restrict__ lam,
-                                                       const float4* __restrict__ grads, float4* __restrict__ out,
-                                                       bool acc) {
+                                                       long long ls4, const float4* __restrict__ grads,
+                                                       float4* __restrict__ out, bool acc) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= N4) return;
     const float ht = 1.f / (float)n_t;
     const long long gs = (long long)d * N4;
-    const float4 l0 = lam[q], ln = lam[(long long)n_t * N4 + q];
+    const float4 l0 = lam[q], ln = lam[(long long)n_t * ls4 + q];
     float4 b[3];
     for (int c = 0; c < d; ++c) {
         const float4 g0 = grads[c * N4 + q], gn = grads[n_t * gs + c * N4 + q];
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(TPB) k_body_force_f4(long long N4, int n_t, in
         b[c].w = 0.5f * ht * (l0.w * g0.w + ln.w * gn.w);
     }
     for (int j = 1; j < n_t; ++j) {
-        const float4 lj = lam[(long long)j * N4 + q];
+        const float4 lj = lam[(long long)j * ls4 + q];
         for (int c = 0; c < d; ++c) {
             const float4 gj = grads[j * gs + c * N4 + q];
             b[c].x += ht * (lj.x * gj.x);
@@ -395,15 +395,17 @@ __global__ void __launch_bounds__(TPB) k_body_force_f4(long long N4, int n_t, in
 }
 
 void body_force(const Dims& g, int tdtype, int odtype, int n_t, const void* lam, const void* grads, void* out,
-                bool accumulate, cudaStream_t st) {
-    if (tdtype == F32 && odtype == F32 && g.N % 4 == 0 &&
+                bool accumulate, cudaStream_t st, long long lam_stride) {
+    if (lam_stride <= 0) lam_stride = g.N;
+    if (tdtype == F32 && odtype == F32 && g.N % 4 == 0 && lam_stride % 4 == 0 &&
         ((((uintptr_t)lam) | ((uintptr_t)grads) | ((uintptr_t)out)) & 15) == 0) {
         const long long N4 = g.N / 4;
-        k_body_force_f4<<<blocks_for(N4, TPB), TPB, 0, st>>>(N4, n_t, g.d, (const float4*)lam, (const float4*)grads,
-                                                             (float4*)out, accumulate);
+        k_body_force_f4<<<blocks_for(N4, TPB), TPB, 0, st>>>(N4, n_t, g.d, (const float4*)lam, lam_stride / 4,
+                                                             (const float4*)grads, (float4*)out, accumulate);
         FRG_CHECK_LAUNCH();
         return;
     }
+    FRG_REQUIRE(lam_stride == g.N, "strided lambda series need the fp32 body force");
     if (tdtype == F64 && odtype == F64)
         k_body_force<double, double><<<vox_grid(g), vox_block(), 0, st>>>(g, n_t, (const double*)lam,
                                                                           (const double*)grads, (double*)out,

@@ -223,9 +223,9 @@ void inc_first(const Dims& g, int method, int n_t, const float* disp, const floa
     const size_t Ns = (size_t)(g.n0 + 2 * g.h0) * g.n1 * g.n2;
     IncFirstOp<float, 3> op;
     op.ds = disp_src(g, disp);
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < 3; ++c) {  // vt_loc == nullptr: the owned planes of vt_src
         op.vtT[c] = vt_src + c * Ns;
-        op.vl[c] = vt_loc + c * g.N;
+        op.vl[c] = vt_loc ? vt_loc + c * g.N : vt_src + c * Ns + (size_t)g.h0 * g.n1 * g.n2;
     }
     op.gy = grads_y;
     op.gx = grads;

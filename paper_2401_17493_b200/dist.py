@@ -304,6 +304,26 @@ class DistKktState:
         self.comm.halo(ext, W)
         return ext
 
+    def _plan(self, disp: torch.Tensor) -> torch.Tensor:
+        """Tile plan of a slab displacement map (the SL steps issue their TMA
+        from it instead of reducing the stencil box per tile)."""
+        plan = torch.empty((L.lib().frg_tile_plan_count(self.n_loc), 4), dtype=torch.int32, device="cuda")
+        L.check(L.lib().frg_tile_plan(self.n_loc, 3, self._m, _c(disp), _c(plan), L.stream()), "tile_plan")
+        return plan
+
+    def _bind(self):
+        """Bind disp_f / disp_b to their plans for the calls that follow."""
+        L.check(L.lib().frg_bind_plan(0, _c(self.disp_f), _c(self.plan_f), self._m), "bind_plan")
+        L.check(L.lib().frg_bind_plan(1, _c(self.disp_b), _c(self.plan_b), self._m), "bind_plan")
+
+    def __del__(self):
+        # drop this state's plan bindings (their maps are about to be freed)
+        try:
+            if L._lib is not None:
+                L.lib().frg_clear_plans()
+        except Exception:
+            pass
+
     def _halo_of(self, disp: torch.Tensor) -> int:
         local = float(disp[0].abs().max().item())
         return max(halo_width(self.comm.all_reduce(local, "max"), self.method), 1)
@@ -379,6 +399,8 @@ class DistKktState:
         self.disp_f, v_ext, Wv = self._departure(v32, 1.0)
         self.disp_b, _, _ = self._departure(v32, -1.0)
         self.Wf, self.Wb = self._halo_of(self.disp_f), self._halo_of(self.disp_b)
+        self.plan_f, self.plan_b = self._plan(self.disp_f), self._plan(self.disp_b)
+        self._bind()
         divv = torch.empty(g.n, dtype=torch.float32, device="cuda")
         L.check(L.lib().frg_slab_fd8_divergence(self.n_loc, g.n_glob[0], Wv, _c(v_ext), _c(divv), L.stream()),
                 "slab_fd8_divergence")
@@ -415,26 +437,42 @@ class DistKktState:
         return _Vec(self.grid, out)
 
     def hessian_matvec(self, vtilde, out: torch.Tensor | None = None) -> _Vec:
-        """kkt.py:237-260 (GN, SSD) on the slab."""
+        """kkt.py:237-260 (GN, SSD) on the slab.  The incremental state and
+        adjoint series are stored with W ghost planes around every slice, so
+        each step writes the owned planes of the next step's source in place
+        and the exchange only fills the ghosts (no interior copy)."""
         g = self.grid
+        self._bind()
+        n0l, plane = g.n0_loc, g.n_glob[1] * g.n_glob[2]
+        Wf, Wb = self.Wf, self.Wb
         vt = vtilde.data if hasattr(vtilde, "data") else vtilde
-        vtT = vt.float()
-        mt = torch.empty((g.n_t + 1, *g.n), dtype=torch.float32, device="cuda")
+        vt_ext = torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
+        vt_ext[:, Wf:Wf + n0l].copy_(vt)  # f64 -> f32 straight into the owned planes
+        self.comm.halo(vt_ext, Wf)
+        mt = torch.empty((g.n_t + 1, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
         S = torch.empty((max(g.n_t - 1, 1), *g.n), dtype=torch.float32, device="cuda")
-        L.check(L.lib().frg_slab_inc_first(self.n_loc, g.n_glob[0], self.Wf, self._m, g.n_t, _c(self.disp_f),
-                                           _c(self.grads), _c(self.grads_y), _c(self._ext(vtT, self.Wf)), _c(vtT),
-                                           _c(mt[1]), _c(S), L.stream()), "slab_inc_first")
+        own_f = lambda j: mt[j, Wf:Wf + n0l]  # noqa: E731
+        L.check(L.lib().frg_slab_inc_first(self.n_loc, g.n_glob[0], Wf, self._m, g.n_t, _c(self.disp_f),
+                                           _c(self.grads), _c(self.grads_y), _c(vt_ext), None, _c(own_f(1)),
+                                           _c(S), L.stream()), "slab_inc_first")
         for j in range(1, g.n_t):
-            L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], self.Wf, self._m, _c(self.disp_f),
-                                              _c(self._ext(mt[j], self.Wf)), _c(S[j - 1]), _c(mt[j + 1]),
-                                              L.stream()), "slab_inc_step")
-        lt = torch.empty_like(mt)
-        torch.neg(mt[g.n_t], out=lt[g.n_t])  # SSD: lam~(1) = -m~(1)
-        self._adjoint(lt)
+            self.comm.halo(mt[j:j + 1], Wf)
+            L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], Wf, self._m, _c(self.disp_f), _c(mt[j]),
+                                              _c(S[j - 1]), _c(own_f(j + 1)), L.stream()), "slab_inc_step")
+        lt = torch.empty((g.n_t + 1, n0l + 2 * Wb, *g.n[1:]), dtype=torch.float32, device="cuda")
+        torch.neg(own_f(g.n_t), out=lt[g.n_t, Wb:Wb + n0l])  # SSD: lam~(1) = -m~(1)
+        for j in range(g.n_t, 0, -1):
+            self.comm.halo(lt[j:j + 1], Wb)
+            L.check(L.lib().frg_slab_adjoint_step(self.n_loc, g.n_glob[0], Wb, self._m, _c(self.disp_b),
+                                                  _c(self.cmul), _c(lt[j]), _c(lt[j - 1, Wb:Wb + n0l]),
+                                                  L.stream()), "slab_adjoint_step")
         self.matvecs += 1
         self.pde_solves += 2
+        b = torch.empty((3, *g.n), dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_slab_body_force(self.n_loc, g.n_t, _c(lt[0, Wb:Wb + n0l]), (n0l + 2 * Wb) * plane,
+                                            _c(self.grads), _c(b), L.stream()), "slab_body_force")
         out = torch.empty((3, *g.n), dtype=torch.float64, device="cuda") if out is None else out
-        self._spectral_out(vt, self._body_force(lt), out)
+        self._spectral_out(vt, b, out)
         return _Vec(g, out)
 
     def apply_precond(self, r, kind: PrecondKind | None = None, outer_tol: float = 0.0,
@@ -460,7 +498,10 @@ class DistKktState:
     def objective_at(self, v_trial) -> float:
         vt = (v_trial.data if hasattr(v_trial, "data") else v_trial).to(torch.float64)
         disp, _, _ = self._departure(vt.float(), 1.0)
+        plan = self._plan(disp)
+        L.check(L.lib().frg_bind_plan(0, _c(disp), _c(plan), self._m), "bind_plan")
         m = self._state_solve(disp, self._halo_of(disp), keep=False)
+        self._bind()
         self.pde_solves += 1
         return self._ssd(m) + self._reg_energy(vt)
 
