@@ -41,7 +41,8 @@ from . import _lib as L
 from .diffops import frg_reg
 from .kkt import PrecondKind, RegConfig
 
-__all__ = ["SlabComm", "SlabGrid", "SlabFFT", "DistKktState", "dist_register", "slab_bounds", "halo_width"]
+__all__ = ["SlabComm", "SlabGrid", "SlabFFT", "DistKktState", "dist_register", "dist_continuation_solve",
+           "slab_bounds", "halo_width"]
 
 TWO_PI = 2.0 * math.pi
 
@@ -528,3 +529,37 @@ def dist_register(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, co
     reg = reg or RegConfig()
     state = DistKktState(m0, m1, reg, comm, n_glob, n_t=n_t, method=method, v_init=v0)
     return solve(state, config or OptimizerConfig(), PrecondKind("reg"), compute_detgrad=False)
+
+
+def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, alpha_target: float,
+                            reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic"):
+    """continuation.continuation_solve (continuation.py:239-293) on the slab
+    decomposition — config C5's alpha cascade 1, 0.1, ..., alpha_target with
+    warm starts, every stage a SPMD dist_register.  Returns (velocity slab,
+    aggregate report, per-stage reports); det(F) statistics are not computed
+    on the slab path (detgrad_* stay 1)."""
+    from dataclasses import replace
+
+    from .continuation import cascade_alphas
+    from .optimizer import OptimizerConfig, SolveReport
+
+    reg = reg or RegConfig()
+    opt = opt or OptimizerConfig()
+    v, stages, total = None, [], SolveReport()
+    for a in cascade_alphas(alpha_target):
+        vv, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=replace(reg, alpha=a), n_t=n_t, method=method,
+                                v0=None if v is None else v.data)
+        v = vv
+        stages.append(rep)
+        total.iterations += rep.iterations
+        total.matvecs += rep.matvecs
+        total.pde_solves += rep.pde_solves
+        total.line_search_evals += rep.line_search_evals
+        total.precond_fallbacks += rep.precond_fallbacks
+        total.runtime += rep.runtime
+    last = stages[-1]
+    total.mismatch, total.gradient = last.mismatch, last.gradient
+    total.status, total.exit_reason = last.status, last.exit_reason
+    total.trace = [row for rep in stages for row in rep.trace]
+    return v, total, stages
+

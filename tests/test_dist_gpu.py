@@ -71,7 +71,7 @@ def _worker(rank, size, port, n, outdir, do_register):
     res["objective_at"] = abs(st.objective_at(1.1 * v[:, lo:hi].contiguous())
                               - ref.objective_at(F.VectorField._wrap(m0.grid, 1.1 * v))) / abs(ref.objective())
     res["mismatch"] = abs(st.mismatch() - ref.mismatch())
-    if do_register:
+    if do_register is True:
         cfg = OptimizerConfig()
         _, rep_d = D.dist_register(m0.values[lo:hi].float(), m1.values[lo:hi].float(), comm, (n, n, n), config=cfg,
                                    reg=reg)
@@ -80,6 +80,16 @@ def _worker(rank, size, port, n, outdir, do_register):
         res["register"] = {"dist": [rep_d.iterations, rep_d.matvecs, rep_d.status],
                            "single": [rep_1.iterations, rep_1.matvecs, rep_1.status],
                            "mismatch": [rep_d.mismatch, rep_1.mismatch]}
+    if do_register == "continuation":
+        from paper_2401_17493_b200.continuation import continuation_solve
+
+        _, tot_d, st_d = D.dist_continuation_solve(m0.values[lo:hi].float(), m1.values[lo:hi].float(), comm,
+                                                  (n, n, n), 1e-2, reg=reg)
+        _, tot_1, st_1 = continuation_solve(m0, m1, 1e-2, reg=reg, precond=F.PrecondKind("reg"),
+                                            transport_dtype=np.float32)
+        res["continuation"] = {"dist": [[r.iterations, r.matvecs] for r in st_d],
+                               "single": [[r.iterations, r.matvecs] for r in st_1],
+                               "status": [tot_d.status, tot_1.status]}
     with open(os.path.join(outdir, f"rank{rank}.json"), "w") as fh:
         json.dump(res, fh)
     tdist.barrier()
@@ -110,3 +120,13 @@ def test_slab_register_matches_single_gpu(tmp_path):
         assert reg["dist"][2] == "converged" == reg["single"][2], reg
         assert reg["dist"][:2] == reg["single"][:2], reg
         assert abs(reg["mismatch"][0] - reg["mismatch"][1]) < 1e-5 * max(reg["mismatch"][1], 1e-3), reg
+
+
+def test_slab_continuation_matches_single_gpu(tmp_path):
+    """Config C5's alpha cascade (1, 0.1, 0.01) on the slab path: same stage
+    iteration and matvec counts as the single-GPU continuation_solve."""
+    for r in _run(2, 64, tmp_path, do_register="continuation"):
+        c = r["continuation"]
+        assert c["status"] == ["converged", "converged"], c
+        assert c["dist"] == c["single"], c
+
