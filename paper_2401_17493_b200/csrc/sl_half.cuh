@@ -49,6 +49,32 @@ __device__ __forceinline__ float row_dot(const unsigned* __restrict__ rw, float2
     return acc.x + acc.y;
 }
 
+// fp16 twin of patch_axis (sl_fast.cuh): only the out-of-range rows / columns
+__device__ __forceinline__ void patch_axis_half(__half* __restrict__ box, const __half* __restrict__ src,
+                                                const Dims& g, int lo0, int lo1, int lo2, int S0, int S1, int S2,
+                                                int axis, int tid) {
+    const int lo = axis == 1 ? lo1 : lo2;
+    const int S = axis == 1 ? S1 : S2;
+    const int n = axis == 1 ? g.n1 : g.n2;
+    const int a_end = lo < 0 ? min(-lo, S) : 0;
+    const int b_beg = lo + S > n ? max(n - lo, 0) : S;
+    const int cnt = a_end + (S - b_beg);
+    if (cnt == 0) return;
+    const int E1 = S0;                    // planes
+    const int E2 = axis == 2 ? S1 : S2;  // the other in-plane extent
+    const int total = cnt * E1 * E2;
+    for (int e = tid; e < total; e += BX * BY) {
+        const int r = e / E2;
+        const int in2 = e - r * E2;
+        const int q = r / E1;
+        const int a = r - q * E1;
+        const int x = q < a_end ? q : b_beg + (q - a_end);
+        const int b = axis == 1 ? x : in2, c = axis == 1 ? in2 : x;
+        const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        box[(a * TB_J + b) * TB_K + c] = src[((size_t)gi * g.n1 + gj) * g.n2 + gk];
+    }
+}
+
 template <int M, class Op>
 __global__ void __launch_bounds__(BX* BY, 4)
     k_slh(Dims g, Op op, const __grid_constant__ TmaMaps<1> maps, const __half* __restrict__ src16) {
@@ -116,16 +142,8 @@ __global__ void __launch_bounds__(BX* BY, 4)
         mbar_wait_sleep(&bar, 0u);
         if (lo1 < 0 || lo1 + S1 > g.n1 || lo2 < 0 || lo2 + S2 > g.n2) {
             // rows / columns leaving the grid: copy from their periodic images
-            const int total = S0 * S1 * S2;
-            for (int e = tid; e < total; e += BX * BY) {
-                int r = e / S2;
-                const int c = e - r * S2;
-                const int a = r / S1;
-                const int b = r - a * S1;
-                if (lo1 + b >= 0 && lo1 + b < g.n1 && lo2 + c >= 0 && lo2 + c < g.n2) continue;
-                const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
-                b0[(a * TB_J + b) * TB_K + c] = src16[((size_t)gi * g.n1 + gj) * g.n2 + gk];
-            }
+            patch_axis_half(b0, src16, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
+            patch_axis_half(b0, src16, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
             __syncthreads();
         }
         // shifted copy: word w of b1 = (b0[2w + 1], b0[2w + 2])
@@ -138,10 +156,9 @@ __global__ void __launch_bounds__(BX* BY, 4)
         __syncthreads();
         const unsigned* W0 = reinterpret_cast<const unsigned*>(b0);
         const unsigned* W1 = reinterpret_cast<const unsigned*>(b1);
+        if (M == LINEAR) {
 #pragma unroll
-        for (int u = 0; u < SL_TI; ++u) {
-            float r = 0.f;
-            if (M == LINEAR) {
+            for (int u = 0; u < SL_TI; ++u) {
                 // taps (c, c + 1) of four rows from the parity-matched copy
                 const int o = ok[u] ? ((base0[u] - lo0) * TB_J + (base1[u] - lo1)) * TB_K + (base2[u] - lo2) : 0;
                 const unsigned* P = ((o & 1) ? W1 : W0) + (o >> 1);
@@ -150,32 +167,46 @@ __global__ void __launch_bounds__(BX* BY, 4)
                              c11 = h2f(P[(TB_PLANE + TB_K) / 2]);
                 const float e00 = (1.f - t2) * c00.x + t2 * c00.y, e01 = (1.f - t2) * c01.x + t2 * c01.y;
                 const float e10 = (1.f - t2) * c10.x + t2 * c10.y, e11 = (1.f - t2) * c11.x + t2 * c11.y;
-                r = (1.f - t0) * ((1.f - t1) * e00 + t1 * e01) + t0 * ((1.f - t1) * e10 + t1 * e11);
-            } else {
-                const int o = ok[u] ? ((base0[u] - 1 - lo0) * TB_J + (base1[u] - 1 - lo1)) * TB_K + (base2[u] - 1 - lo2)
-                                    : 0;
-                const unsigned* P = ((o & 1) ? W1 : W0) + (o >> 1);
-                float w0[4], w1[4], w2[4];
-                if (M == BSPLINE) {
-                    bspline4(fr0[u], w0);
-                    bspline4(fr1[u], w1);
-                    bspline4(fr2[u], w2);
-                } else {
-                    lagrange4f(fr0[u], w0);
-                    lagrange4f(fr1[u], w1);
-                    lagrange4f(fr2[u], w2);
-                }
-                const float2 w01 = make_float2(w2[0], w2[1]), w23 = make_float2(w2[2], w2[3]);
+                vals[u][0] = (1.f - t0) * ((1.f - t1) * e00 + t1 * e01) + t0 * ((1.f - t1) * e10 + t1 * e11);
+            }
+        } else {
+            // two voxels per paired FMA, as the fp32 engine: each stencil row is
+            // two half2 words per voxel, converted straight into the (A, B)
+            // register pairs of FFMA2
+#pragma unroll
+            for (int u = 0; u < SL_TI; u += 2) {
+                const int oA = ok[u] ? ((base0[u] - 1 - lo0) * TB_J + (base1[u] - 1 - lo1)) * TB_K +
+                                           (base2[u] - 1 - lo2)
+                                     : 0;
+                const int oB = ok[u + 1] ? ((base0[u + 1] - 1 - lo0) * TB_J + (base1[u + 1] - 1 - lo1)) * TB_K +
+                                               (base2[u + 1] - 1 - lo2)
+                                         : 0;
+                const unsigned* PA = ((oA & 1) ? W1 : W0) + (oA >> 1);
+                const unsigned* PB = ((oB & 1) ? W1 : W0) + (oB >> 1);
+                float2 w0[4], w1[4], w2[4];
+                weights4f_x2<M>(make_float2(fr0[u], fr0[u + 1]), w0);
+                weights4f_x2<M>(make_float2(fr1[u], fr1[u + 1]), w1);
+                weights4f_x2<M>(make_float2(fr2[u], fr2[u + 1]), w2);
+                float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
-                    float plane = 0.f;
+                    float2 plane = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) plane = fmaf(w1[b], row_dot(P + (a * TB_PLANE + b * TB_K) / 2, w01, w23),
-                                                             plane);
-                    r = fmaf(w0[a], plane, r);
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const int ro = (a * TB_PLANE + bb * TB_K) / 2;
+                        const float2 a01 = h2f(PA[ro]), a23 = h2f(PA[ro + 1]);
+                        const float2 b01 = h2f(PB[ro]), b23 = h2f(PB[ro + 1]);
+                        float2 r = __fmul2_rn(w2[0], make_float2(a01.x, b01.x));
+                        r = __ffma2_rn(w2[1], make_float2(a01.y, b01.y), r);
+                        r = __ffma2_rn(w2[2], make_float2(a23.x, b23.x), r);
+                        r = __ffma2_rn(w2[3], make_float2(a23.y, b23.y), r);
+                        plane = __ffma2_rn(w1[bb], r, plane);
+                    }
+                    acc = __ffma2_rn(w0[a], plane, acc);
                 }
+                vals[u][0] = acc.x;
+                vals[u + 1][0] = acc.y;
             }
-            vals[u][0] = r;
         }
     } else {
         // the box does not fit: fp32 gathers from global memory (rare)
