@@ -42,6 +42,24 @@ __device__ __forceinline__ float2 h2f(unsigned w) {
     return __half22float2(h);
 }
 
+__device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<unsigned*>(&h); }
+
+// f16 x f16 + f32 -> f32 (one FHFMA; the compiler folds the half selection
+// into .H0 / .H1 operand selectors)
+__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
+    float r;
+    asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(r) : "h"(a), "h"(b), "f"(c));
+    return r;
+}
+
+// one stencil row: taps t01 = (c, c+1), t23 = (c+2, c+3), weights likewise
+__device__ __forceinline__ float row_fhfma(unsigned t01, unsigned t23, unsigned w01, unsigned w23) {
+    float r = fhfma((unsigned short)(w01 & 0xffffu), (unsigned short)(t01 & 0xffffu), 0.f);
+    r = fhfma((unsigned short)(w01 >> 16), (unsigned short)(t01 >> 16), r);
+    r = fhfma((unsigned short)(w23 & 0xffffu), (unsigned short)(t23 & 0xffffu), r);
+    return fhfma((unsigned short)(w23 >> 16), (unsigned short)(t23 >> 16), r);
+}
+
 // one stencil row: taps (c, c+1, c+2, c+3) as two half2 words -> w . taps
 __device__ __forceinline__ float row_dot(const unsigned* __restrict__ rw, float2 w01, float2 w23) {
     float2 acc = __fmul2_rn(w01, h2f(rw[0]));
@@ -92,6 +110,7 @@ __global__ void __launch_bounds__(BX* BY, 4)
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    __syncthreads();  // barrier initialised before anyone waits on it (nothing in flight yet)
     const int4 pe = __ldg(op.ds.plan + (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
     bool ok[SL_TI];
     float dsp[SL_TI][3];
@@ -123,7 +142,6 @@ __global__ void __launch_bounds__(BX* BY, 4)
                 "r"(smem_u32(&bar))
                 : "memory");
     }
-    __syncthreads();  // barrier initialised before anyone waits on it
 
     int base0[SL_TI], base1[SL_TI], base2[SL_TI];
     float fr0[SL_TI], fr1[SL_TI], fr2[SL_TI];
@@ -187,6 +205,13 @@ __global__ void __launch_bounds__(BX* BY, 4)
                 weights4f_x2<M>(make_float2(fr0[u], fr0[u + 1]), w0);
                 weights4f_x2<M>(make_float2(fr1[u], fr1[u + 1]), w1);
                 weights4f_x2<M>(make_float2(fr2[u], fr2[u + 1]), w2);
+                // x-direction weights as fp16 pairs: each stencil row is 4
+                // FHFMA (f16 x f16 + f32 accumulate, .H0/.H1 operand
+                // selectors: no conversions), rows / planes combine in fp32
+                const unsigned wA01 = h2u(__floats2half2_rn(w2[0].x, w2[1].x)),
+                               wA23 = h2u(__floats2half2_rn(w2[2].x, w2[3].x));
+                const unsigned wB01 = h2u(__floats2half2_rn(w2[0].y, w2[1].y)),
+                               wB23 = h2u(__floats2half2_rn(w2[2].y, w2[3].y));
                 float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
@@ -194,13 +219,9 @@ __global__ void __launch_bounds__(BX* BY, 4)
 #pragma unroll
                     for (int bb = 0; bb < 4; ++bb) {
                         const int ro = (a * TB_PLANE + bb * TB_K) / 2;
-                        const float2 a01 = h2f(PA[ro]), a23 = h2f(PA[ro + 1]);
-                        const float2 b01 = h2f(PB[ro]), b23 = h2f(PB[ro + 1]);
-                        float2 r = __fmul2_rn(w2[0], make_float2(a01.x, b01.x));
-                        r = __ffma2_rn(w2[1], make_float2(a01.y, b01.y), r);
-                        r = __ffma2_rn(w2[2], make_float2(a23.x, b23.x), r);
-                        r = __ffma2_rn(w2[3], make_float2(a23.y, b23.y), r);
-                        plane = __ffma2_rn(w1[bb], r, plane);
+                        const float rA = row_fhfma(PA[ro], PA[ro + 1], wA01, wA23);
+                        const float rB = row_fhfma(PB[ro], PB[ro + 1], wB01, wB23);
+                        plane = __ffma2_rn(w1[bb], make_float2(rA, rB), plane);
                     }
                     acc = __ffma2_rn(w0[a], plane, acc);
                 }

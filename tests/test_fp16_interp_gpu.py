@@ -32,6 +32,7 @@ def test_fp16_interp_matches_f64(method, order):
     r = ref.hessian_matvec(vt).data
     e16 = _rel(h16.hessian_matvec(vt).data, r)
     e32 = _rel(h32.hessian_matvec(vt).data, r)
+    print(f"fp16 interpolation ({method}): matvec rel-L2 {e16:.2e} vs f64 (fp32: {e32:.2e})")
     assert e16 < 1e-3, e16
     assert e32 < 1e-5, e32
     assert e16 > e32  # the fp16 taps are really used
