@@ -399,6 +399,7 @@ def run_slab(a, F, world, rank, barrier, max_over_ranks):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
+    b0 = comm.bytes_sent
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(steps):
@@ -407,9 +408,18 @@ def run_slab(a, F, world, rank, barrier, max_over_ranks):
     torch.cuda.synchronize()
     barrier()
     t = max_over_ranks(s0.elapsed_time(s1)) / 1e3
+    sent = (comm.bytes_sent - b0) / steps  # NVLink payload per matvec per rank (halo + all-to-all)
+    canon = 174 * 4 * n ** 3 / world       # SURVEY 8d canonical HBM bytes per matvec per rank
+    peak, _ = peaks()
     return {"workload": f"C4: one {n}^3 GN Hessian matvec slab-decomposed over {world} ranks", "grid": [n] * 3,
             "ranks": world, "value": steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps, "steps": steps,
             "scaling": "strong", "halo_planes": [st.Wf, st.Wb],
+            "nvlink_bytes_per_step_per_rank": sent,
+            "nvlink_roofline": {"achieved_gbs": sent / (t / steps) / 1e9, "peak_gbs": 900.0,
+                                "frac": sent / (t / steps) / 900e9, "note": "payload sent per rank / step time"},
+            "hbm_roofline": {"achieved_gbs": canon / (t / steps) / 1e9, "peak_gbs": peak,
+                             "frac": canon / (t / steps) / 1e9 / peak,
+                             "note": "SURVEY 8d canonical 174 fp32 field passes per matvec, per rank"},
             "parallelism": f"slab along axis 0 x{world}: NCCL all-to-all FFT transposes, ghost-plane send/recv"}
 
 

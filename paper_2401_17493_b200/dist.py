@@ -74,6 +74,7 @@ class SlabComm:
         self.rank = tdist.get_rank(group)
         self.size = tdist.get_world_size(group)
         self.staged = tdist.get_backend(group) != "nccl"
+        self.bytes_sent = 0  # payload this rank sent (halo planes + all-to-all chunks to other ranks)
 
     # -- scalars -----------------------------------------------------------
     def all_reduce(self, value: float, op: str = "sum") -> float:
@@ -91,6 +92,7 @@ class SlabComm:
             return
         if out.is_complex():  # NCCL has no complex type: move the (re, im) pairs as reals
             out, inp = torch.view_as_real(out), torch.view_as_real(inp)
+        self.bytes_sent += inp.numel() * inp.element_size() * (self.size - 1) // self.size
         if self.staged:
             o = torch.empty(out.shape, dtype=out.dtype)
             tdist.all_to_all_single(o, inp.cpu(), group=self.group)
@@ -114,6 +116,7 @@ class SlabComm:
         prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
         send_lo = ext[:, W:2 * W].contiguous()          # my first planes -> prev's upper ghosts
         send_hi = ext[:, n0l:n0l + W].contiguous()      # my last planes  -> next's lower ghosts
+        self.bytes_sent += 2 * send_lo.numel() * send_lo.element_size()
         recv_hi = torch.empty_like(send_lo)
         recv_lo = torch.empty_like(send_hi)
         if self.staged:
