@@ -133,6 +133,11 @@ int frg_body_force(const int32_t n[3], int32_t d, int32_t dtype, int32_t n_t, co
 int frg_deformation_tensor(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, int32_t n_t,
                            const void* disp, const void* jac, void* F, void* stream);
 int frg_determinant(const int32_t n[3], int32_t d, int32_t dtype, const void* F, void* det, void* stream);
+/* one Heun step of d_t F = (grad v) F at every voxel of a 3D grid (or slab):
+ * first != 0: F = I + h/2 (J_y + J (I + h J_y)); else F holds F_j(y) on entry
+ * and is updated in place (jac_y, jac, F: 9 x N)                transport.py:197-221 */
+int frg_deform_update(const int32_t n[3], int32_t dtype, double h_t, int32_t first, const void* jac_y,
+                      const void* jac, void* F, void* stream);
 /* composed departure displacement over n_t steps                           transport.py:224-247 */
 int frg_compose(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, int32_t n_t, const void* disp,
                 void* out, void* stream);
@@ -204,8 +209,12 @@ int frg_kkt_detgrad(frg_kkt* k, double out[3]);
  * axis 0.  Arrays named *_src carry h0 ghost planes before and after the
  * owned planes per component ((n_loc[0] + 2 h0) planes, filled by the caller's
  * halo exchange); all other arrays are (n_loc[0], n1, n2).  fp32 transport,
- * linear or cubic.  The host (dist.py) exchanges ghost planes and runs the
- * all-to-all transposes between these calls.
+ * linear, cubic or B-spline.  For FRG_BSPLINE every *_src array holds the
+ * B-spline COEFFICIENTS of its field (the prefilter is global: the caller runs
+ * it with the slab FFT and frg_slab_spec_apply(FRG_SYM_BSPLINE_PREFILTER)
+ * before the halo exchange); *_loc arrays keep the nodal values.  The host
+ * (dist.py) exchanges ghost planes and runs the all-to-all transposes between
+ * these calls.
  * ------------------------------------------------------------------------- */
 int frg_slab_departure(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, double h_t,
                        const void* v_src, const void* v_loc, void* disp, void* stream);

@@ -64,6 +64,7 @@ PROTOTYPES = {
     "frg_body_force": [_N3, _I, _I, _I, _P, _P, _P, _P],
     "frg_deformation_tensor": [_N3, _I, _I, _I, _I, _P, _P, _P, _P],
     "frg_determinant": [_N3, _I, _I, _P, _P, _P],
+    "frg_deform_update": [_N3, _I, ctypes.c_double, _I, _P, _P, _P, _P],
     "frg_compose": [_N3, _I, _I, _I, _I, _P, _P, _P],
     "frg_fd8_gradient": [_N3, _I, _I, _I, _P, _P, _P],
     "frg_fd8_divergence": [_N3, _I, _I, _P, _P, _P],

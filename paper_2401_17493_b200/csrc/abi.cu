@@ -207,6 +207,14 @@ int frg_deformation_tensor(const int32_t n[3], int32_t d, int32_t dtype, int32_t
     });
 }
 
+int frg_deform_update(const int32_t n[3], int32_t dtype, double h_t, int32_t first, const void* jac_y,
+                      const void* jac, void* F, void* stream) {
+    return guard([&] {
+        check_dtype(dtype);
+        deform_update(dims_of(n, 3), dtype, h_t, first != 0, jac_y, jac, F, ST(stream));
+    });
+}
+
 int frg_determinant(const int32_t n[3], int32_t d, int32_t dtype, const void* F, void* det, void* stream) {
     return guard([&] {
         check_dtype(dtype);
@@ -495,12 +503,15 @@ int frg_kkt_detgrad(frg_kkt* k, double out[3]) {
 static Dims slab_dims(const int32_t n_loc[3], int32_t n0_glob, int32_t h0) {
     FRG_REQUIRE(n_loc != nullptr && n_loc[0] >= 1 && n_loc[1] >= 1 && n_loc[2] >= 1, "bad slab grid");
     FRG_REQUIRE(n0_glob >= n_loc[0] && h0 >= 0, "bad slab decomposition");
+    FRG_REQUIRE(h0 >= 1, "slab sources carry at least one ghost plane");
     Dims g = make_dims(n_loc, 3);
     g.h0 = h0;
     g.n0g = n0_glob;
     return g;
 }
-static void check_slab_method(int m) { FRG_REQUIRE(m == 1 || m == 2, "slab transport: linear or cubic (B-spline needs the global prefilter)"); }
+static void check_slab_method(int m) {
+    FRG_REQUIRE(m == FRG_LINEAR || m == FRG_CUBIC || m == FRG_BSPLINE, "slab transport: linear, cubic or B-spline");
+}
 
 extern "C" {
 

@@ -60,6 +60,8 @@ void body_force(const Dims& g, int tdtype, int odtype, int n_t, const void* lam,
 void deformation_tensor(const Dims& g, int tdtype, int method, int n_t, const void* disp,
                         const void* jac, void* F, void* work, cudaStream_t st);
 void determinant(const Dims& g, int tdtype, const void* F, void* det, cudaStream_t st);
+void deform_update(const Dims& g, int tdtype, double ht, bool first, const void* jac_y, const void* jac, void* F,
+                   cudaStream_t st);
 // composed departure displacement over n_t steps
 void compose_disp(const Dims& g, int tdtype, int method, int n_t, const void* disp, void* out,
                   void* work, cudaStream_t st);

@@ -281,14 +281,15 @@ void* bspline_scratch(int slot, size_t bytes);
 // Every SL launch: fp32 linear / cubic / B-spline gathers of fp32 fields take
 // the TMA engine (single-field steps the fp16-tap engine when the host thread
 // selected 16-bit interpolation and the map has a tile plan), everything else (f64 parity path, nearest, converting
-// sources) the generic staged engine of sl_tile.cuh.  BSPLINE first replaces
-// every gathered source by its prefiltered coefficients.
+// sources) the generic staged engine of sl_tile.cuh.  BSPLINE on a whole grid
+// first replaces every gathered source by its prefiltered coefficients; on a
+// slab (h0 > 0) the sources already are coefficients (the prefilter is a
+// global FFT the host ran before the halo exchange, include/flowreg_b200.h).
 template <typename T, int NF, class Op>
 void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
     Op op = op_in;
-    if (method == BSPLINE) {
+    if (method == BSPLINE && g.h0 == 0) {
         using V = typename Op::V;
-        FRG_REQUIRE(g.h0 == 0, "B-spline transport needs the global prefilter (single-GPU grids)");
         for (int f = 0; f < NF; ++f) {
             V* c = (V*)bspline_scratch(f, sizeof(V) * (size_t)g.N);
             bspline_prefilter(g, tcode(V(0)), op.field(f), c, st);

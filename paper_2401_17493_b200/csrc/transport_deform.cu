@@ -89,6 +89,29 @@ static void deformation_d(const Dims& g, int method, int n_t, const T* disp, con
     }
 }
 
+// one pointwise Heun update of F (first: F_y = I, F written; else F holds
+// F_j(y) and is updated in place) — the slab path's deformation step
+void deform_update(const Dims& g, int tdtype, double ht, bool first, const void* jac_y, const void* jac, void* F,
+                   cudaStream_t st) {
+    FRG_REQUIRE(g.d == 3, "deform_update: 3D");
+    if (tdtype == F64) {
+        if (first)
+            k_deform_first<double, 3><<<vox_grid(g), vox_block(), 0, st>>>(g, ht, (const double*)jac_y,
+                                                                           (const double*)jac, (double*)F);
+        else
+            k_deform_step<double, 3><<<vox_grid(g), vox_block(), 0, st>>>(g, ht, (const double*)jac_y,
+                                                                          (const double*)jac, (double*)F);
+    } else {
+        if (first)
+            k_deform_first<float, 3><<<vox_grid(g), vox_block(), 0, st>>>(g, (float)ht, (const float*)jac_y,
+                                                                          (const float*)jac, (float*)F);
+        else
+            k_deform_step<float, 3><<<vox_grid(g), vox_block(), 0, st>>>(g, (float)ht, (const float*)jac_y,
+                                                                         (const float*)jac, (float*)F);
+    }
+    FRG_CHECK_LAUNCH();
+}
+
 void deformation_tensor(const Dims& g, int tdtype, int method, int n_t, const void* disp, const void* jac, void* F,
                         void* work, cudaStream_t st) {
     if (tdtype == F64) {

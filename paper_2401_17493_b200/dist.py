@@ -42,7 +42,7 @@ from .diffops import frg_reg
 from .kkt import PrecondKind, RegConfig
 
 __all__ = ["SlabComm", "SlabGrid", "SlabFFT", "DistKktState", "dist_register", "dist_continuation_solve",
-           "slab_bounds", "halo_width"]
+           "dist_search_alpha", "slab_bounds", "halo_width"]
 
 TWO_PI = 2.0 * math.pi
 
@@ -58,8 +58,8 @@ def slab_bounds(n0: int, nranks: int, rank: int) -> tuple[int, int]:
 def halo_width(max_abs_disp0: float, method: str = "cubic") -> int:
     """Ghost planes a gather needs for axis-0 displacements |d0| <= max_abs_disp0
     (index units): stencil planes floor(d0) - 1 .. floor(d0) + 2 for cubic,
-    floor(d0) .. floor(d0) + 1 for linear."""
-    extra = 2 if method == "cubic" else 1
+    floor(d0) .. floor(d0) + 1 for linear (B-spline: the cubic support)."""
+    extra = 1 if method == "linear" else 2
     return int(math.ceil(max(float(max_abs_disp0), 0.0))) + extra
 
 
@@ -82,7 +82,8 @@ class SlabComm:
             return float(value)
         dev = "cpu" if self.staged else torch.device("cuda", torch.cuda.current_device())
         t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.SUM if op == "sum" else tdist.ReduceOp.MAX, group=self.group)
+        ops = {"sum": tdist.ReduceOp.SUM, "max": tdist.ReduceOp.MAX, "min": tdist.ReduceOp.MIN}
+        tdist.all_reduce(t, op=ops[op], group=self.group)
         return float(t.item())
 
     # -- all-to-all with equal chunks along dim 0 -------------------------
@@ -264,7 +265,10 @@ class _Vec:
 
 class DistKktState:
     """Slab-decomposed counterpart of kkt.KktState (kkt.py:136-341) for SSD,
-    FD8, linear / cubic fp32 transport, fp64 control vectors.
+    FD8, linear / cubic / B-spline fp32 transport, fp64 control vectors.
+    B-spline: every gathered field is first prefiltered globally (slab FFT,
+    symbol 1 / prod_a (4 + 2 cos(2 pi m_a / n_a)) / 6) and its coefficients
+    exchanged; nodal values stay where the kernels read them locally.
 
     Same methods and counters as KktState (refresh, gradient, hessian_matvec,
     apply_precond('reg'), objective, objective_at, mismatch), each a sequence
@@ -272,13 +276,14 @@ class DistKktState:
 
     def __init__(self, m0: torch.Tensor, m1: torch.Tensor, reg: RegConfig, comm: SlabComm, n_glob, n_t: int = 4,
                  method: str = "cubic", v_init: torch.Tensor | None = None):
-        if method not in ("linear", "cubic"):
-            raise ValueError("slab transport supports linear / cubic interpolation")
+        if method not in ("linear", "cubic", "bspline"):
+            raise ValueError("slab transport supports linear / cubic / bspline interpolation")
         self.comm = comm
         self.grid = SlabGrid(tuple(int(v) for v in n_glob), comm.rank, comm.size, n_t=n_t)
         self.reg = reg
         self.method = method
         self._m = L.METHODS[method]
+        self._bs = method == "bspline"
         self._reg = frg_reg(reg.operator, reg.alpha, reg.incomp)
         self._project = reg.incomp.mode != "none"
         # H1: spectral part in fp32 (as the single-GPU fast path); H2/H3 fp64
@@ -307,6 +312,18 @@ class DistKktState:
         ext[:, W:W + n0l].copy_(x)
         self.comm.halo(ext, W)
         return ext
+
+    def _coef(self, x: torch.Tensor) -> torch.Tensor:
+        """What a gather reads of field x: x itself, or (B-spline) its global
+        prefilter coefficients."""
+        if not self._bs:
+            return x
+        xx = x if x.dim() == 4 else x.unsqueeze(0)
+        return self.fft.apply(xx.contiguous(), "bspline_prefilter", self._reg).view(x.shape)
+
+    def _src(self, x: torch.Tensor, W: int) -> torch.Tensor:
+        """Ghost-extended gather source of x (coefficients for B-spline)."""
+        return self._ext(self._coef(x), W)
 
     def _plan(self, disp: torch.Tensor) -> torch.Tensor:
         """Tile plan of a slab displacement map (the SL steps issue their TMA
@@ -360,7 +377,7 @@ class DistKktState:
         h0 = TWO_PI / self.grid.n_glob[0]
         Wv = max(halo_width(self.comm.all_reduce(float(vs[0].abs().max().item()) * self.grid.h_t / h0, "max"),
                             self.method), 4)
-        v_ext = self._ext(vs, Wv)
+        v_ext = self._src(vs, Wv)
         disp = torch.empty_like(vs)
         L.check(L.lib().frg_slab_departure(self.n_loc, self.grid.n_glob[0], Wv, self._m, self.grid.h_t, _c(v_ext),
                                            _c(vs), _c(disp), L.stream()), "slab_departure")
@@ -372,7 +389,7 @@ class DistKktState:
         series = [m] if keep else None
         for _ in range(g.n_t):
             nxt = torch.empty_like(m)
-            self._gather(disp, W, [self._ext(m, W)], [nxt])
+            self._gather(disp, W, [self._src(m, W)], [nxt])
             m = nxt
             if keep:
                 series.append(m)
@@ -406,6 +423,8 @@ class DistKktState:
         self.plan_f, self.plan_b = self._plan(self.disp_f), self._plan(self.disp_b)
         self._bind()
         divv = torch.empty(g.n, dtype=torch.float32, device="cuda")
+        if self._bs:  # the departure solve exchanged coefficients; FD8 needs the nodal values
+            v_ext = self._ext(v32, Wv)
         L.check(L.lib().frg_slab_fd8_divergence(self.n_loc, g.n_glob[0], Wv, _c(v_ext), _c(divv), L.stream()),
                 "slab_fd8_divergence")
         self.mseries = self._state_solve(self.disp_f, self.Wf, keep=True)
@@ -416,11 +435,11 @@ class DistKktState:
                                                   _c(self.grads[j]), L.stream()), "slab_fd8_gradient")
         self.grads_y = torch.empty((g.n_t, 3, *g.n), dtype=torch.float32, device="cuda")
         for j in range(g.n_t):
-            ext = self._ext(self.grads[j], self.Wf)
+            ext = self._src(self.grads[j], self.Wf)
             self._gather(self.disp_f, self.Wf, [ext[c] for c in range(3)], [self.grads_y[j, c] for c in range(3)])
         self.cmul = torch.empty(g.n, dtype=torch.float32, device="cuda")
         L.check(L.lib().frg_slab_adjoint_multiplier(self.n_loc, g.n_glob[0], self.Wb, self._m, g.h_t,
-                                                    _c(self.disp_b), _c(self._ext(divv, self.Wb)), _c(divv),
+                                                    _c(self.disp_b), _c(self._src(divv, self.Wb)), _c(divv),
                                                     _c(self.cmul), L.stream()), "slab_adjoint_multiplier")
         self.lam = torch.empty((g.n_t + 1, *g.n), dtype=torch.float32, device="cuda")
         torch.sub(self.m1, self.mseries[-1], out=self.lam[g.n_t])  # -(m(1) - m1), SSD
@@ -432,7 +451,7 @@ class DistKktState:
         g = self.grid
         for j in range(g.n_t, 0, -1):
             L.check(L.lib().frg_slab_adjoint_step(self.n_loc, g.n_glob[0], self.Wb, self._m, _c(self.disp_b),
-                                                  _c(self.cmul), _c(self._ext(series[j], self.Wb)),
+                                                  _c(self.cmul), _c(self._src(series[j], self.Wb)),
                                                   _c(series[j - 1]), L.stream()), "slab_adjoint_step")
 
     def gradient(self) -> _Vec:
@@ -450,25 +469,37 @@ class DistKktState:
         n0l, plane = g.n0_loc, g.n_glob[1] * g.n_glob[2]
         Wf, Wb = self.Wf, self.Wb
         vt = vtilde.data if hasattr(vtilde, "data") else vtilde
-        vt_ext = torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
-        vt_ext[:, Wf:Wf + n0l].copy_(vt)  # f64 -> f32 straight into the owned planes
-        self.comm.halo(vt_ext, Wf)
+        if self._bs:  # gathers read exchanged coefficients; the Heun terms the nodal v~
+            vt_loc = vt.to(torch.float32).contiguous()
+            vt_ext, vt_loc_p = self._src(vt_loc, Wf), _c(vt_loc)
+        else:
+            vt_ext = torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
+            vt_ext[:, Wf:Wf + n0l].copy_(vt)  # f64 -> f32 straight into the owned planes
+            self.comm.halo(vt_ext, Wf)
+            vt_loc_p = None
         mt = torch.empty((g.n_t + 1, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
         S = torch.empty((max(g.n_t - 1, 1), *g.n), dtype=torch.float32, device="cuda")
         own_f = lambda j: mt[j, Wf:Wf + n0l]  # noqa: E731
         L.check(L.lib().frg_slab_inc_first(self.n_loc, g.n_glob[0], Wf, self._m, g.n_t, _c(self.disp_f),
-                                           _c(self.grads), _c(self.grads_y), _c(vt_ext), None, _c(own_f(1)),
+                                           _c(self.grads), _c(self.grads_y), _c(vt_ext), vt_loc_p, _c(own_f(1)),
                                            _c(S), L.stream()), "slab_inc_first")
+
+        def source(series, j, W):  # ghost-extended gather source of slice j
+            if self._bs:
+                return self._src(series[j, W:W + n0l], W)
+            self.comm.halo(series[j:j + 1], W)
+            return series[j]
+
         for j in range(1, g.n_t):
-            self.comm.halo(mt[j:j + 1], Wf)
-            L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], Wf, self._m, _c(self.disp_f), _c(mt[j]),
+            src = source(mt, j, Wf)
+            L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], Wf, self._m, _c(self.disp_f), _c(src),
                                               _c(S[j - 1]), _c(own_f(j + 1)), L.stream()), "slab_inc_step")
         lt = torch.empty((g.n_t + 1, n0l + 2 * Wb, *g.n[1:]), dtype=torch.float32, device="cuda")
         torch.neg(own_f(g.n_t), out=lt[g.n_t, Wb:Wb + n0l])  # SSD: lam~(1) = -m~(1)
         for j in range(g.n_t, 0, -1):
-            self.comm.halo(lt[j:j + 1], Wb)
+            src = source(lt, j, Wb)
             L.check(L.lib().frg_slab_adjoint_step(self.n_loc, g.n_glob[0], Wb, self._m, _c(self.disp_b),
-                                                  _c(self.cmul), _c(lt[j]), _c(lt[j - 1, Wb:Wb + n0l]),
+                                                  _c(self.cmul), _c(src), _c(lt[j - 1, Wb:Wb + n0l]),
                                                   L.stream()), "slab_adjoint_step")
         self.matvecs += 1
         self.pde_solves += 2
@@ -520,18 +551,90 @@ class DistKktState:
         return 0.0
 
     def detgrad_stats(self):
-        return 1.0, 1.0, 1.0
+        """(min, mean, max) of det F(1) over the whole grid (kkt.py
+        detgrad, transport.py:197-221 on the slab): jac = FD8 grad v, its
+        gather at the feet, n_t Heun steps of d_t F = (grad v) F (9-field
+        slab gathers of F + the pointwise update), det, all-reduced."""
+        g = self.grid
+        n0l = g.n0_loc
+        W = max(self.Wf, 4)
+        v32 = self.v.data.float()
+        jac = torch.empty((3, 3, *g.n), dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_slab_fd8_gradient(self.n_loc, g.n_glob[0], W, 3, _c(self._ext(v32, W)), _c(jac),
+                                              L.stream()), "slab_fd8_gradient")
+        jac9 = jac.view(9, *g.n)
+        jac_y = torch.empty_like(jac9)
+        ext = self._src(jac9, self.Wf)
+        self._bind()
+        self._gather(self.disp_f, self.Wf, [ext[e] for e in range(9)], [jac_y[e] for e in range(9)])
+        F = torch.empty_like(jac9)
+        L.check(L.lib().frg_deform_update(self.n_loc, L.F32, g.h_t, 1, _c(jac_y), _c(jac9), _c(F), L.stream()),
+                "deform_update")
+        for _ in range(1, g.n_t):
+            ext = self._src(F, self.Wf)
+            self._gather(self.disp_f, self.Wf, [ext[e] for e in range(9)], [F[e] for e in range(9)])
+            L.check(L.lib().frg_deform_update(self.n_loc, L.F32, g.h_t, 0, _c(jac_y), _c(jac9), _c(F), L.stream()),
+                    "deform_update")
+        det = torch.empty(g.n, dtype=torch.float32, device="cuda")
+        L.check(L.lib().frg_determinant(self.n_loc, 3, L.F32, _c(F), _c(det), L.stream()), "determinant")
+        mms = (ctypes.c_double * 3)()
+        L.check(L.lib().frg_min_max_sum(L.F32, _c(det), det.numel(), mms, L.stream()), "min_max_sum")
+        dmin = self.comm.all_reduce(float(mms[0]), "min")
+        dmax = self.comm.all_reduce(float(mms[1]), "max")
+        dsum = self.comm.all_reduce(float(mms[2]))
+        return dmin, dsum / float(np.prod(g.n_glob)), dmax
 
 
 def dist_register(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, config=None, reg: RegConfig | None = None,
-                  n_t: int = 4, method: str = "cubic", v0: torch.Tensor | None = None):
+                  n_t: int = 4, method: str = "cubic", v0: torch.Tensor | None = None, compute_detgrad: bool = True):
     """optimizer.register (optimizer.py:174-281) on the slab decomposition:
     the same host control, SPMD on every rank, reductions all-reduced."""
     from .optimizer import OptimizerConfig, solve
 
     reg = reg or RegConfig()
     state = DistKktState(m0, m1, reg, comm, n_glob, n_t=n_t, method=method, v_init=v0)
-    return solve(state, config or OptimizerConfig(), PrecondKind("reg"), compute_detgrad=False)
+    return solve(state, config or OptimizerConfig(), PrecondKind("reg"), compute_detgrad=compute_detgrad)
+
+
+def dist_search_alpha(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, cfg=None,
+                      reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic"):
+    """continuation.search_alpha (continuation.py:87-207) on the slab
+    decomposition: the same sweep / bisection (continuation.run_search), every
+    trial a SPMD dist_register warm-started from the previous trial unless the
+    warm objective exceeds the cold one; det F(1) bounds from the slab
+    deformation solve (DistKktState.detgrad_stats).  Returns a SearchResult
+    whose velocities are this rank's slabs."""
+    from dataclasses import replace
+
+    from .continuation import SearchConfig, TrialRecord, run_search
+    from .optimizer import OptimizerConfig
+
+    cfg = cfg or SearchConfig()
+    reg = reg or RegConfig()
+    opt = opt or OptimizerConfig()
+
+    def trial(alpha, v_warm, phase):
+        reg_a = replace(reg, alpha=alpha)
+        v0, warm_started, dropped = (None if v_warm is None else v_warm.data), v_warm is not None, False
+        if v_warm is not None:  # continuation.py:98-108: drop a warm start worse than v = 0
+            st = DistKktState(m0, m1, reg_a, comm, n_glob, n_t=n_t, method=method, v_init=v0)
+            if st.objective() > st._init_mismatch:
+                v0, warm_started, dropped = None, False, True
+            del st
+        v, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=reg_a, n_t=n_t, method=method, v0=v0)
+        ok = rep.detgrad_min > cfg.eps_det and rep.detgrad_max < 1.0 / cfg.eps_det
+        rec = TrialRecord(alpha=alpha, passed=ok, det_min=rep.detgrad_min, det_max=rep.detgrad_max,
+                          det_mean=rep.detgrad_mean, mismatch=rep.mismatch, iterations=rep.iterations,
+                          warm_started=warm_started, warm_start_dropped=dropped, phase=phase)
+        return v, rec
+
+    def is_zero(v):
+        out = ctypes.c_double()
+        L.check(L.lib().frg_norm_inf(L.F64, L.ptr(v.data), v.data.numel(), ctypes.byref(out), L.stream()),
+                "norm_inf")
+        return comm.all_reduce(out.value, "max") == 0.0
+
+    return run_search(cfg, trial, is_zero)
 
 
 def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, alpha_target: float,
@@ -539,8 +642,8 @@ def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, 
     """continuation.continuation_solve (continuation.py:239-293) on the slab
     decomposition — config C5's alpha cascade 1, 0.1, ..., alpha_target with
     warm starts, every stage a SPMD dist_register.  Returns (velocity slab,
-    aggregate report, per-stage reports); det(F) statistics are not computed
-    on the slab path (detgrad_* stay 1)."""
+    aggregate report, per-stage reports); det F(1) statistics of the last
+    stage as in continuation_solve."""
     from dataclasses import replace
 
     from .continuation import cascade_alphas
@@ -549,9 +652,10 @@ def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, 
     reg = reg or RegConfig()
     opt = opt or OptimizerConfig()
     v, stages, total = None, [], SolveReport()
-    for a in cascade_alphas(alpha_target):
+    alphas = cascade_alphas(alpha_target)
+    for a in alphas:
         vv, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=replace(reg, alpha=a), n_t=n_t, method=method,
-                                v0=None if v is None else v.data)
+                                v0=None if v is None else v.data, compute_detgrad=(a == alphas[-1]))
         v = vv
         stages.append(rep)
         total.iterations += rep.iterations
@@ -563,6 +667,7 @@ def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, 
     last = stages[-1]
     total.mismatch, total.gradient = last.mismatch, last.gradient
     total.status, total.exit_reason = last.status, last.exit_reason
+    total.detgrad_min, total.detgrad_mean, total.detgrad_max = last.detgrad_min, last.detgrad_mean, last.detgrad_max
     total.trace = [row for rep in stages for row in rep.trace]
     return v, total, stages
 

@@ -39,7 +39,7 @@ def _rel(a, b):
     return float((a - b).norm() / max(float(b.norm()), 1e-300))
 
 
-def _worker(rank, size, port, n, outdir, do_register):
+def _worker(rank, size, port, n, outdir, do_register, method):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as tdist
@@ -56,11 +56,11 @@ def _worker(rank, size, port, n, outdir, do_register):
     v = 0.5 * vtrue.data
     gen = torch.Generator(device="cuda").manual_seed(0)
     vt = 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=torch.float64, device="cuda")
-    ref = F.KktState(m0, m1, reg, v_init=F.VectorField._wrap(m0.grid, v), transport_dtype=np.float32)
+    ref = F.KktState(m0, m1, reg, v_init=F.VectorField._wrap(m0.grid, v), transport_dtype=np.float32, method=method)
     comm = D.SlabComm()
     lo, hi = D.slab_bounds(n, size, rank)
     st = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
-                        v_init=v[:, lo:hi].contiguous())
+                        v_init=v[:, lo:hi].contiguous(), method=method)
     res["gradient"] = _rel(st.gradient().data, ref.gradient().data[:, lo:hi])
     res["matvec"] = _rel(st.hessian_matvec(vt[:, lo:hi].contiguous()).data,
                          ref.hessian_matvec(F.VectorField._wrap(m0.grid, vt)).data[:, lo:hi])
@@ -90,16 +90,30 @@ def _worker(rank, size, port, n, outdir, do_register):
         res["continuation"] = {"dist": [[r.iterations, r.matvecs] for r in st_d],
                                "single": [[r.iterations, r.matvecs] for r in st_1],
                                "status": [tot_d.status, tot_1.status]}
+    if do_register == "search":
+        from paper_2401_17493_b200.continuation import SearchConfig, search_alpha
+
+        cfg = SearchConfig(eps_det=0.5, bisection_depth=2)
+        plain = F.RegConfig(alpha=1.0)
+        r_d = D.dist_search_alpha(m0.values[lo:hi].float(), m1.values[lo:hi].float(), comm, (n, n, n), cfg=cfg,
+                                  reg=plain, method=method)
+        r_1 = search_alpha(m0, m1, cfg=cfg, reg=plain, precond=F.PrecondKind("reg"), method=method,
+                           transport_dtype=np.float32)
+        row = lambda t: [t.alpha, t.passed, t.iterations, t.warm_started, t.phase]  # noqa: E731
+        det = lambda t: [t.det_min, t.det_mean, t.det_max]  # noqa: E731
+        res["search"] = {"dist": [row(t) for t in r_d.trials], "single": [row(t) for t in r_1.trials],
+                         "det_dist": [det(t) for t in r_d.trials], "det_single": [det(t) for t in r_1.trials],
+                         "best": [r_d.alpha, r_1.alpha], "status": [r_d.status, r_1.status]}
     with open(os.path.join(outdir, f"rank{rank}.json"), "w") as fh:
         json.dump(res, fh)
     tdist.barrier()
     tdist.destroy_process_group()
 
 
-def _run(size, n, tmp_path, do_register=False):
+def _run(size, n, tmp_path, do_register=False, method="cubic"):
     import torch.multiprocessing as mp
 
-    mp.start_processes(_worker, args=(size, _free_port(), n, str(tmp_path), do_register), nprocs=size,
+    mp.start_processes(_worker, args=(size, _free_port(), n, str(tmp_path), do_register, method), nprocs=size,
                        start_method="spawn", join=True)
     return [json.load(open(os.path.join(tmp_path, f"rank{r}.json"))) for r in range(size)]
 
@@ -109,6 +123,17 @@ def test_slab_kkt_matches_single_gpu(size, tmp_path):
     for rank, res in enumerate(_run(size, 64, tmp_path)):
         for key in ("gradient", "matvec", "precond"):
             assert res[key] < 1e-5, (size, rank, key, res[key])
+        assert res["objective"] < 1e-6 and res["objective_at"] < 1e-6, res
+        assert res["mismatch"] < 1e-6, res
+
+
+@pytest.mark.parametrize("method", ["bspline", "linear"])
+def test_slab_kkt_methods_match_single_gpu(method, tmp_path):
+    """B-spline on the slab: global prefilter through the slab FFT, exchanged
+    coefficients, nodal values local — same tolerances as cubic."""
+    for rank, res in enumerate(_run(2, 64, tmp_path, method=method)):
+        for key in ("gradient", "matvec", "precond"):
+            assert res[key] < 1e-5, (method, rank, key, res[key])
         assert res["objective"] < 1e-6 and res["objective_at"] < 1e-6, res
         assert res["mismatch"] < 1e-6, res
 
@@ -130,3 +155,15 @@ def test_slab_continuation_matches_single_gpu(tmp_path):
         assert c["status"] == ["converged", "converged"], c
         assert c["dist"] == c["single"], c
 
+
+
+def test_slab_search_alpha_matches_single_gpu(tmp_path):
+    """search_alpha (continuation.py:144-207) on the slab: the same trials
+    (alpha, pass / fail, iterations, warm starts), det F(1) statistics from the
+    slab deformation solve within 1e-4 of the single-GPU ones."""
+    for r in _run(2, 64, tmp_path, do_register="search"):
+        s = r["search"]
+        assert len(s["dist"]) >= 2 and s["dist"] == s["single"], s
+        assert s["best"][0] == s["best"][1] and s["status"][0] == s["status"][1], s
+        for a, b in zip(s["det_dist"], s["det_single"]):
+            assert np.allclose(a, b, rtol=1e-4, atol=1e-6), (a, b)
