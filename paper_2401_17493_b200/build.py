@@ -43,7 +43,9 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str | None 
     lib = out or LIB
     if out is None and not force and not needs_build():
         return LIB
-    objdir = os.path.join(os.path.dirname(lib), "_build") if out else os.path.join(HERE, "_build")
+    # variants compile into their own object directory (never the default's)
+    objdir = (os.path.join(os.path.dirname(lib), "_build_" + os.path.basename(lib).replace(".so", "")) if out
+              else os.path.join(HERE, "_build"))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -298,7 +298,10 @@ __device__ __forceinline__ A apply_stencil(const V* __restrict__ f, const Stenci
 // voxel launch geometry: block (32, 8) over (k, j), grid z over i.  No
 // integer division anywhere; the flat index fits in 32 bits.
 // ---------------------------------------------------------------------------
-constexpr int BX = 32, BY = 8;
+#ifndef FRG_BY
+#define FRG_BY 8
+#endif
+constexpr int BX = 32, BY = FRG_BY;
 
 struct Vox {
     int i, j, k, p;
