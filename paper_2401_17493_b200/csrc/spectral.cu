@@ -822,11 +822,16 @@ __global__ void k_slab_spec_scale(Dims g, int i1_off, int n1_loc, int ncomp, C* 
     }
 }
 
-// a = alpha sym a + P(b), both normalised (k_spec_combine on the split spectrum)
-template <typename C>
-__global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, C* __restrict__ a, const C* __restrict__ bsp,
+// out = alpha sym a + P(b), both normalised (k_spec_combine on the split
+// spectrum); out may alias a or b (every input of a bin is read before its
+// output is written); arithmetic in the output's precision (an f64 bin of a
+// rounded to fp32 keeps its per-bin relative accuracy: the symbol multiplies
+// the rounded value, it does not amplify global rounding)
+template <typename CA, typename CB = CA, typename CO = CA>
+__global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, const CA* a, const CB* bsp, CO* out,
                                RegSpec r, double invN, bool have_a, bool project) {
-    using M = typename CR<C>::R;
+    using M = typename CR<CO>::R;
+    using RO = typename CR<CO>::R;
     const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
          e += (long long)gridDim.x * blockDim.x) {
@@ -843,9 +848,9 @@ __global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, C* __restrict__ a
         }
         M br[3], bi[3], k[3] = {M(0), M(0), M(0)}, mfac = M(0);
         for (int c = 0; c < g.d; ++c) {
-            C v = bsp[(long long)c * cnt + e];
-            br[c] = v.x;
-            bi[c] = v.y;
+            const CB v = bsp[(long long)c * cnt + e];
+            br[c] = M(v.x);
+            bi[c] = M(v.y);
         }
         if (project && r.incomp != 0) {
             for (int q = 0; q < 3; ++q) k[q] = bn.nyq[q] ? M(0) : M(bn.m[q]);
@@ -871,14 +876,14 @@ __global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, C* __restrict__ a
             M orr = (br[c] - kc * mfac * dr) * iN;
             M oi = (bi[c] - kc * mfac * di) * iN;
             if (have_a) {
-                C av = a[(long long)c * cnt + e];
-                orr += sa * av.x;
-                oi += sa * av.y;
+                const CA av = a[(long long)c * cnt + e];
+                orr += sa * M(av.x);
+                oi += sa * M(av.y);
             }
-            C o;
-            o.x = orr;
-            o.y = oi;
-            a[(long long)c * cnt + e] = o;
+            CO o;
+            o.x = RO(orr);
+            o.y = RO(oi);
+            out[(long long)c * cnt + e] = o;
         }
     }
 }
@@ -904,10 +909,12 @@ void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a
     const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
     if (dtype == F64)
         k_slab_combine<cufftDoubleComplex><<<slab_blocks(cnt), 256, 0, st>>>(
-            g, i1_off, n1_loc, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, r, invN, a != b, project);
+            g, i1_off, n1_loc, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, (cufftDoubleComplex*)a, r, invN,
+            a != b, project);
     else
         k_slab_combine<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, i1_off, n1_loc, (cufftComplex*)a,
-                                                                     (const cufftComplex*)b, r, invN, a != b, project);
+                                                                     (const cufftComplex*)b, (cufftComplex*)a, r,
+                                                                     invN, a != b, project);
     FRG_CHECK_LAUNCH();
 }
 
@@ -923,11 +930,46 @@ void slab_combine_flat(const Dims& g, void* a, const void* b, const RegSpec& r, 
     const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
     if (f64)
         k_slab_combine<cufftDoubleComplex><<<slab_blocks(cnt), 256, 0, st>>>(
-            g, 0, g.n1, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, r, invN, have_a, project);
+            g, 0, g.n1, (cufftDoubleComplex*)a, (const cufftDoubleComplex*)b, (cufftDoubleComplex*)a, r, invN,
+            have_a, project);
     else
         k_slab_combine<cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(g, 0, g.n1, (cufftComplex*)a,
-                                                                     (const cufftComplex*)b, r, invN, have_a, project);
+                                                                     (const cufftComplex*)b, (cufftComplex*)a, r,
+                                                                     invN, have_a, project);
     FRG_CHECK_LAUNCH();
+}
+
+// Mixed-precision alpha L a + P(b) (3D): a (f64) -> D2Z, b (fp32) -> R2C, the
+// combine in f64 arithmetic written as an fp32 spectrum over b's, one C2R
+// into out (fp32).  The forward transform of a must be f64: fp32 rounding of
+// a smooth field (its own and the FFT's, ~1e-7 of |a| spread over every bin)
+// is amplified by alpha |k|^2 at the high frequencies, 4x per grid doubling
+// (measured 3.6e-4 rel-L2 on the 256^3 gradient); after the symbol is
+// applied the inverse rounds relative to |out| only, so fp32 suffices there.
+void mixed_forward_a(PlanCache& pc, void* ws_a, const Dims& g, const double* a, cudaStream_t st) {
+    FRG_REQUIRE(g.d == 3, "reg_plus_project_mixed: 3D");
+    fwd<double>(pc, g, g.d, a, (cufftDoubleComplex*)ws_a, st);
+}
+
+// second half: ws_a already holds the D2Z spectrum of a (mixed_forward_a,
+// possibly issued on another stream the caller has joined)
+void reg_plus_project_mixed_b(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const float* b, float* out,
+                              const RegSpec& r, bool project, cudaStream_t st) {
+    auto* sa = (cufftDoubleComplex*)ws_a;
+    auto* sb = (cufftComplex*)ws_b;
+    fwd<float>(pc, g, g.d, b, sb, st);
+    const long long cnt = (long long)g.n0 * g.n1 * (g.n2 / 2 + 1);
+    const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
+    k_slab_combine<cufftDoubleComplex, cufftComplex, cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(
+        g, 0, g.n1, sa, sb, sb, r, invN, true, project);
+    FRG_CHECK_LAUNCH();
+    inv<float>(pc, g, g.d, sb, out, st);
+}
+
+void reg_plus_project_mixed(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const double* a, const float* b,
+                            float* out, const RegSpec& r, bool project, cudaStream_t st) {
+    mixed_forward_a(pc, ws_a, g, a, st);
+    reg_plus_project_mixed_b(pc, ws_a, ws_b, g, b, out, r, project, st);
 }
 
 }  // namespace frg

@@ -35,6 +35,13 @@ size_t spectral_ws_bytes(const Dims& g, int dtype, int ncomp);
 size_t restrict_ws_bytes(const Dims& gf, int dtype);
 void spectral_apply_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, int ncomp, const void* in, void* out,
                        int kind, const RegSpec& r, cudaStream_t st);
+// mixed precision alpha L a + P(b): a f64 (D2Z), b / out fp32 (spectral.cu)
+void reg_plus_project_mixed(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const double* a, const float* b,
+                            float* out, const RegSpec& r, bool project, cudaStream_t st);
+// the same in two halves: the D2Z of a (any stream), then b's part
+void mixed_forward_a(PlanCache& pc, void* ws_a, const Dims& g, const double* a, cudaStream_t st);
+void reg_plus_project_mixed_b(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, const float* b, float* out,
+                              const RegSpec& r, bool project, cudaStream_t st);
 // out = alpha L a + P[b] (project_on) or alpha L a + b; ws_a/ws_b hold d half spectra each
 void reg_plus_project_ex(PlanCache& pc, void* ws_a, void* ws_b, const Dims& g, int adtype, const void* a,
                          int bdtype, const void* b, void* out, const RegSpec& r, bool project_on, cudaStream_t st);

@@ -286,8 +286,10 @@ class DistKktState:
         self._bs = method == "bspline"
         self._reg = frg_reg(reg.operator, reg.alpha, reg.incomp)
         self._project = reg.incomp.mode != "none"
-        # H1: spectral part in fp32 (as the single-GPU fast path); H2/H3 fp64
-        self._spec_dt = torch.float32 if reg.operator.order == 1 else torch.float64
+        # spectral operators on f64 spectra: fp32 rounding of a smooth field is
+        # amplified by alpha |k|^2 at high frequencies (4x per grid doubling,
+        # 3.6e-4 rel-L2 on a 256^3 gradient), see kkt.cu mixed_spectral
+        self._spec_dt = torch.float64
         self.fft = SlabFFT(self.grid, comm)
         g = self.grid
         self.n_loc = L.n3(g.n)
