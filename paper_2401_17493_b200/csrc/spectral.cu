@@ -846,11 +846,19 @@ __global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, const CA* a, cons
             for (int o = 1; o < r.order; ++o) s *= base;
             sa = M(r.alpha) * s * M(invN);
         }
-        M br[3], bi[3], k[3] = {M(0), M(0), M(0)}, mfac = M(0);
+        // every input of the bin is loaded before the first store (out may
+        // alias a or b, so later loads could not be hoisted above a store)
+        M br[3], bi[3], ar[3] = {M(0), M(0), M(0)}, ai[3] = {M(0), M(0), M(0)}, k[3] = {M(0), M(0), M(0)},
+                                mfac = M(0);
         for (int c = 0; c < g.d; ++c) {
             const CB v = bsp[(long long)c * cnt + e];
             br[c] = M(v.x);
             bi[c] = M(v.y);
+            if (have_a) {
+                const CA av = a[(long long)c * cnt + e];
+                ar[c] = M(av.x);
+                ai[c] = M(av.y);
+            }
         }
         if (project && r.incomp != 0) {
             for (int q = 0; q < 3; ++q) k[q] = bn.nyq[q] ? M(0) : M(bn.m[q]);
@@ -876,9 +884,8 @@ __global__ void k_slab_combine(Dims g, int i1_off, int n1_loc, const CA* a, cons
             M orr = (br[c] - kc * mfac * dr) * iN;
             M oi = (bi[c] - kc * mfac * di) * iN;
             if (have_a) {
-                const CA av = a[(long long)c * cnt + e];
-                orr += sa * M(av.x);
-                oi += sa * M(av.y);
+                orr += sa * ar[c];
+                oi += sa * ai[c];
             }
             CO o;
             o.x = RO(orr);
