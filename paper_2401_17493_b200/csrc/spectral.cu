@@ -247,11 +247,20 @@ __global__ void k_spec_scale(Dims g, long long nh, int ncomp, C* __restrict__ x,
     Bin b = bin_of(g, i0, i1, i2);
     double s = symbol_of(g, b, kind, r) * invN;
     using R = typename CR<C>::R;
-    for (int c = 0; c < ncomp; ++c) {
-        C v = x[(long long)c * nh + p];
-        v.x = (R)(v.x * s);
-        v.y = (R)(v.y * s);
-        x[(long long)c * nh + p] = v;
+    // three components per round: their loads all issue before the stores
+    // (in place, so a later load could not be hoisted above an earlier store)
+    for (int c0 = 0; c0 < ncomp; c0 += 3) {
+        C v[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c0 + c < ncomp) v[c] = x[(long long)(c0 + c) * nh + p];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c0 + c < ncomp) {
+                v[c].x = (R)(v[c].x * s);
+                v[c].y = (R)(v[c].y * s);
+                x[(long long)(c0 + c) * nh + p] = v[c];
+            }
     }
 }
 

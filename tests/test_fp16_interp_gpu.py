@@ -30,12 +30,16 @@ def test_fp16_interp_matches_f64(method, order):
     vt = F.VectorField._wrap(m0.grid, 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=torch.float64,
                                                        device="cuda"))
     r = ref.hessian_matvec(vt).data
-    e16 = _rel(h16.hessian_matvec(vt).data, r)
-    e32 = _rel(h32.hessian_matvec(vt).data, r)
+    o16 = h16.hessian_matvec(vt).data
+    o32 = h32.hessian_matvec(vt).data
+    e16, e32 = _rel(o16, r), _rel(o32, r)
     print(f"fp16 interpolation ({method}): matvec rel-L2 {e16:.2e} vs f64 (fp32: {e32:.2e})")
     assert e16 < 1e-3, e16
     assert e32 < 1e-5, e32
-    assert e16 > e32  # the fp16 taps are really used
+    # the fp16 taps are really used (with H2 the alpha L part dominates the
+    # random direction's matvec, so the transport difference can sit below the
+    # fp32 inverse-FFT rounding in e16 vs e32)
+    assert not torch.equal(o16, o32)
     # state / adjoint / gradient keep fp32 taps: identical to the fp32 context
     assert torch.equal(h16.gradient().data, h32.gradient().data)
     assert h16.objective() == h32.objective()
