@@ -22,6 +22,37 @@ def test_slab_bounds_and_halo_width():
     # cubic stencil planes floor(d) - 1 .. floor(d) + 2
     assert halo_width(0.0) == 2 and halo_width(0.5) == 3 and halo_width(3.0) == 5
     assert halo_width(0.5, "linear") == 2
+    assert halo_width(0.5, "bspline") == halo_width(0.5, "cubic")  # same 4-point support
+
+
+def test_run_search_control_flow():
+    """continuation.run_search — the sweep / bisection of continuation.py:144-207
+    shared by search_alpha and dist_search_alpha — on a mock trial that passes
+    iff alpha >= 3e-3: decades 1, 0.1, 0.01 pass, 1e-3 fails, then bisection
+    between 1e-3 and 1e-2 with warm starts from the previous trial."""
+    from paper_2401_17493_b200.continuation import SearchConfig, TrialRecord, run_search
+
+    seen = []
+
+    def trial(alpha, v_warm, phase):
+        seen.append((alpha, v_warm, phase))
+        ok = alpha >= 3e-3
+        return f"v{len(seen)}", TrialRecord(alpha, ok, 0.5, 1.5, 1.0, 0.1, 3, v_warm is not None, False, phase)
+
+    res = run_search(SearchConfig(bisection_depth=3), trial, lambda v: False)
+    alphas = [a for a, _, _ in seen]
+    assert np.allclose(alphas, [1.0, 0.1, 0.01, 0.001, 0.0055, 0.00325, 0.002125])
+    assert [ph for _, _, ph in seen] == ["sweep"] * 4 + ["bisection"] * 3
+    assert [w for _, w, _ in seen] == [None, "v1", "v2", "v3", "v4", "v5", "v6"]
+    assert res.status == "ok" and np.isclose(res.alpha, 0.00325) and res.velocity == "v6"
+    assert res.anomalies == []
+    # failing at the first alpha, and running into the floor
+    r0 = run_search(SearchConfig(), lambda a, w, ph: (None, TrialRecord(a, False, 0, 0, 0, 0, 1, False, False, ph)),
+                    lambda v: False)
+    assert r0.status == "violated_at_start" and r0.alpha is None and len(r0.trials) == 1
+    r1 = run_search(SearchConfig(alpha_floor=1e-3),
+                    lambda a, w, ph: ("v", TrialRecord(a, True, 1, 1, 1, 0, 1, False, False, ph)), lambda v: False)
+    assert r1.status == "floor_reached" and np.isclose(r1.alpha, 1e-3) and len(r1.trials) == 4
 
 
 def _port():
