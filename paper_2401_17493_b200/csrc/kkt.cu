@@ -48,6 +48,8 @@ struct KktCtx {
     cudaStream_t st;
     PlanCache& plans = shared_plans();
     Workspace ws_a, ws_b, ws_c;
+    bool obj_valid = false;  // objective() of the current (images, velocity), cached until refresh
+    double obj_val = 0.0;
     DevBuf m0, m1, v, vT, negv, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
     DevBuf vtT, vty, mt, lt, bf, disp_trial, mtrial, gmC, tmp1, tmp2, tmp3;
     DevBuf plan_f, plan_b, plan_t;  // SL tile plans of disp_f / disp_b / disp_trial (fp32 maps)
@@ -190,6 +192,7 @@ static void incremental_final_ncc(KktCtx* k, const void* mt, const void* md, voi
 }
 
 void kkt_set_images(KktCtx* k, const void* m0, const void* m1, int dtype) {
+    k->obj_valid = false;
     convert(dtype, m0, k->tdt, k->m0.p, k->N(), k->st);
     convert(dtype, m1, k->tdt, k->m1.p, k->N(), k->st);
     k->tmp1.alloc(k->N() * k->T());
@@ -243,6 +246,7 @@ void kkt_set_interp_bits(KktCtx* k, int bits) {
 
 void kkt_refresh(KktCtx* k, const void* v) {
     FRG_REQUIRE(k->have_images, "set_images must precede refresh");
+    k->obj_valid = false;
     const long long N = k->N(), d = k->g.d;
     const size_t T = k->T(), C = k->C();
     cudaStream_t st = k->st;
@@ -300,7 +304,13 @@ static double reg_energy_c(KktCtx* k, const void* vC) {
 
 double kkt_objective(KktCtx* k) {
     FRG_REQUIRE(k->have_state, "refresh first");
-    return current_dist(k) + reg_energy_c(k, k->v.p);
+    // the optimizer asks for J(v) several times per Newton iteration; the
+    // value only changes with refresh / set_images (kkt.py:188-190)
+    if (!k->obj_valid) {
+        k->obj_val = current_dist(k) + reg_energy_c(k, k->v.p);
+        k->obj_valid = true;
+    }
+    return k->obj_val;
 }
 
 double kkt_objective_at(KktCtx* k, const void* v_trial) {
