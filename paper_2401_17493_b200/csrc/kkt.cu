@@ -15,23 +15,71 @@
 #include "kkt.h"
 #include "sl_half.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace frg {
 
 static size_t es(int dt) { return dt == F64 ? 8 : 4; }
+
+// Process-wide recycling of context buffers: a registration creates a KKT
+// context per solve (and search_alpha / continuation one per trial), each
+// with ~30 grid-sized buffers; cudaMalloc / cudaFree of those cost 15-30 ms
+// per context at 256^3.  Released buffers are kept by size and handed to the
+// next context (after a device synchronise, so no queued kernel still uses
+// them), the way a caching allocator would.
+struct BufPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_list;
+};
+static BufPool& buf_pool() {
+    static BufPool* p = new BufPool();  // intentionally leaked: outlives every context
+    return *p;
+}
+static void* pool_get(size_t& b) {
+    BufPool& bp = buf_pool();
+    {
+        std::lock_guard<std::mutex> lk(bp.mu);
+        auto it = bp.free_list.lower_bound(b);
+        if (it != bp.free_list.end() && it->first <= b + b / 4) {
+            void* p = it->second;
+            b = it->first;
+            bp.free_list.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, b) != cudaSuccess) {
+        // out of memory with buffers parked: give them back and retry once
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(bp.mu);
+        for (auto& e : bp.free_list) cudaFree(e.second);
+        bp.free_list.clear();
+        FRG_CUDA(cudaMalloc(&p, b));
+    }
+    return p;
+}
+static void pool_put(void* p, size_t b) {
+    std::lock_guard<std::mutex> lk(buf_pool().mu);
+    buf_pool().free_list.emplace(b, p);
+}
 
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
     void alloc(size_t b) {
         if (b > bytes) {
-            if (p) cudaFree(p);
-            p = nullptr;
-            FRG_CUDA(cudaMalloc(&p, b));
+            if (p) {
+                FRG_CUDA(cudaDeviceSynchronize());  // queued work may still read the old buffer
+                pool_put(p, bytes);
+            }
+            p = pool_get(b);
             bytes = b;
         }
     }
+    // caller has synchronised (kkt_destroy)
     void free_() {
-        if (p) cudaFree(p);
+        if (p) pool_put(p, bytes);
         p = nullptr;
         bytes = 0;
     }
@@ -125,6 +173,7 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
 
 void kkt_destroy(KktCtx* k) {
     if (!k) return;
+    cudaDeviceSynchronize();  // the buffers go back to the pool for the next context
     DevBuf* bufs[] = {&k->m0, &k->m1, &k->v, &k->vT, &k->negv, &k->disp_f, &k->disp_b, &k->divv, &k->cmul,
                       &k->mseries, &k->grads, &k->grads_y, &k->lam, &k->vtT, &k->vty, &k->mt, &k->lt, &k->bf,
                       &k->disp_trial, &k->mtrial, &k->gmC, &k->tmp1, &k->tmp2, &k->tmp3, &k->c_gm, &k->c_w,
