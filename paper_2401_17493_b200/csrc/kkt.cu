@@ -98,7 +98,7 @@ struct KktCtx {
     Workspace ws_a, ws_b, ws_c;
     bool obj_valid = false;  // objective() of the current (images, velocity), cached until refresh
     double obj_val = 0.0;
-    DevBuf m0, m1, v, vT, negv, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
+    DevBuf m0, m1, v, vT, disp_f, disp_b, divv, cmul, mseries, grads, grads_y, lam;
     DevBuf vtT, vty, mt, lt, bf, disp_trial, mtrial, gmC, tmp1, tmp2, tmp3;
     DevBuf plan_f, plan_b, plan_t;  // SL tile plans of disp_f / disp_b / disp_trial (fp32 maps)
     int interp_bits = 32;           // 16: fp16-tap SL steps (mixed-precision interpolation mode)
@@ -148,7 +148,6 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
     k->m1.alloc(N * T);
     k->v.alloc(d * N * C);
     k->vT.alloc(d * N * T);
-    k->negv.alloc(d * N * T);
     k->disp_f.alloc(d * N * T);
     k->disp_b.alloc(d * N * T);
     k->divv.alloc(N * T);
@@ -174,7 +173,7 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
 void kkt_destroy(KktCtx* k) {
     if (!k) return;
     cudaDeviceSynchronize();  // the buffers go back to the pool for the next context
-    DevBuf* bufs[] = {&k->m0, &k->m1, &k->v, &k->vT, &k->negv, &k->disp_f, &k->disp_b, &k->divv, &k->cmul,
+    DevBuf* bufs[] = {&k->m0, &k->m1, &k->v, &k->vT, &k->disp_f, &k->disp_b, &k->divv, &k->cmul,
                       &k->mseries, &k->grads, &k->grads_y, &k->lam, &k->vtT, &k->vty, &k->mt, &k->lt, &k->bf,
                       &k->disp_trial, &k->mtrial, &k->gmC, &k->tmp1, &k->tmp2, &k->tmp3, &k->c_gm, &k->c_w,
                       &k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q, &k->c_u, &k->plan_f, &k->plan_b,
@@ -303,8 +302,10 @@ void kkt_refresh(KktCtx* k, const void* v) {
     // vT = v in transport precision (departure + divergence)
     convert(k->cdt, k->v.p, k->tdt, k->vT.p, d * N, st);
     departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->vT.p, k->disp_f.p, st);   // kkt.py:171
-    axpby(k->tdt, -1.0, k->vT.p, 0.0, k->negv.p, d * N, st);
-    departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->negv.p, k->disp_b.p, st); // kkt.py:172
+    // departure map of -v (kkt.py:172) without a negated copy: the step -h_t
+    // flips the sign of every displacement and of the gathered v, which is
+    // bit-identical to transporting a negated field
+    departure(k->g, k->tdt, k->tdt, k->method, -1.0 / k->n_t, k->vT.p, k->disp_b.p, st);
     PlanScope pf(0, k->disp_f.p, build_plan(k, k->disp_f.p, k->plan_f), k->method);
     PlanScope pb(1, k->disp_b.p, build_plan(k, k->disp_b.p, k->plan_b), k->method);
     if (k->scheme == 0)                                                                     // kkt.py:173
