@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_div(Dims g, const T* __restrict
 // tile of the current plane with a 4-wide halo: ~3.5 loads per voxel instead
 // of 25 (mostly L2 re-reads of neighbouring planes).  Same per-term order as
 // fd8_line, so results are identical.
-constexpr int FD8_CHUNK = 16;
+#ifndef FRG_FD8_CHUNK
+#define FRG_FD8_CHUNK 16
+#endif
+constexpr int FD8_CHUNK = FRG_FD8_CHUNK;
 
 template <typename T>
 __device__ __forceinline__ T fd8_taps(const T (&up)[5], const T (&um)[5], T inv840h) {
