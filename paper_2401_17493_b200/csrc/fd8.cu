@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_div(Dims g, const T* __restrict
 // of 25 (mostly L2 re-reads of neighbouring planes).  Same per-term order as
 // fd8_line, so results are identical.
 #ifndef FRG_FD8_CHUNK
-#define FRG_FD8_CHUNK 16
+#define FRG_FD8_CHUNK 32
 #endif
 constexpr int FD8_CHUNK = FRG_FD8_CHUNK;
 
