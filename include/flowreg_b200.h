@@ -170,6 +170,9 @@ int frg_pcg_update(int32_t dtype, double k, const void* s, const void* hs, void*
 /* ---- wide boundary: KktState (kkt.py:136-341) ------------------------------ */
 int frg_kkt_create(const frg_config* cfg, void* stream, frg_kkt** out);
 int frg_kkt_destroy(frg_kkt* k);
+/* Destroyed contexts park their device buffers for the next context (capped
+   at FRG_POOL_CAP_MB, default 1/4 of device memory); this frees them all. */
+int frg_release_pool(void);
 int frg_kkt_set_stream(frg_kkt* k, void* stream);
 /* images m0, m1 (N values, dtype) — copied into the context             kkt.py:139-162 */
 /* Interpolation precision of the SL steps of the GN Hessian matvec: 32

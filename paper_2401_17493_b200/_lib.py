@@ -75,6 +75,7 @@ PROTOTYPES = {
     "frg_restrict": [_N3, _I, _P, _P, _P],
     "frg_prolong": [_N3, _I, _P, _P, _P],
     "frg_dot": [_I, _P, _P, _L, _DP, _P],
+    "frg_release_pool": [],
     "frg_norm_inf": [_I, _P, _L, _DP, _P],
     "frg_min_max_sum": [_I, _P, _L, _DP, _P],
     "frg_all_finite": [_I, _P, _L, ctypes.POINTER(ctypes.c_int32), _P],

@@ -360,6 +360,10 @@ int frg_kkt_create(const frg_config* cfg, void* stream, frg_kkt** out) {
     });
 }
 
+int frg_release_pool(void) {
+    return guard([&] { kkt_release_pool(); });
+}
+
 int frg_kkt_destroy(frg_kkt* k) {
     return guard([&] {
         if (!k) return;

@@ -28,22 +28,60 @@ static size_t es(int dt) { return dt == F64 ? 8 : 4; }
 // per context at 256^3.  Released buffers are kept by size and handed to the
 // next context (after a device synchronise, so no queued kernel still uses
 // them), the way a caching allocator would.
+// Parked bytes are capped (FRG_POOL_CAP_MB, default 1/4 of the device's
+// memory; a buffer released past the cap is freed) and keyed by device, and
+// frg_release_pool() hands everything back (the torch caching allocator
+// cannot reclaim memory parked here).
 struct BufPool {
     std::mutex mu;
-    std::multimap<size_t, void*> free_list;
+    std::multimap<std::pair<int, size_t>, void*> free_list;
+    size_t parked = 0;
+    size_t cap = 0;
 };
 static BufPool& buf_pool() {
     static BufPool* p = new BufPool();  // intentionally leaked: outlives every context
     return *p;
 }
+static int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+static size_t pool_cap() {
+    BufPool& bp = buf_pool();
+    if (!bp.cap) {
+        if (const char* e = getenv("FRG_POOL_CAP_MB")) {
+            bp.cap = (size_t)atoll(e) << 20;
+        } else {
+            size_t fr = 0, tot = 0;
+            bp.cap = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot / 4 : ((size_t)16 << 30);
+        }
+        if (!bp.cap) bp.cap = 1;
+    }
+    return bp.cap;
+}
+static void pool_release_all() {
+    BufPool& bp = buf_pool();
+    std::lock_guard<std::mutex> lk(bp.mu);
+    int d0 = cur_device();
+    for (auto& e : bp.free_list) {
+        cudaSetDevice(e.first.first);
+        cudaFree(e.second);
+    }
+    cudaSetDevice(d0);
+    bp.free_list.clear();
+    bp.parked = 0;
+}
 static void* pool_get(size_t& b) {
     BufPool& bp = buf_pool();
+    const int dev = cur_device();
     {
         std::lock_guard<std::mutex> lk(bp.mu);
-        auto it = bp.free_list.lower_bound(b);
-        if (it != bp.free_list.end() && it->first <= b + b / 4) {
+        auto it = bp.free_list.lower_bound({dev, b});
+        if (it != bp.free_list.end() && it->first.first == dev && it->first.second <= b + b / 4) {
             void* p = it->second;
-            b = it->first;
+            b = it->first.second;
+            bp.parked -= b;
             bp.free_list.erase(it);
             return p;
         }
@@ -52,17 +90,24 @@ static void* pool_get(size_t& b) {
     if (cudaMalloc(&p, b) != cudaSuccess) {
         // out of memory with buffers parked: give them back and retry once
         cudaGetLastError();
-        std::lock_guard<std::mutex> lk(bp.mu);
-        for (auto& e : bp.free_list) cudaFree(e.second);
-        bp.free_list.clear();
+        pool_release_all();
         FRG_CUDA(cudaMalloc(&p, b));
     }
     return p;
 }
 static void pool_put(void* p, size_t b) {
-    std::lock_guard<std::mutex> lk(buf_pool().mu);
-    buf_pool().free_list.emplace(b, p);
+    BufPool& bp = buf_pool();
+    const size_t cap = pool_cap();
+    std::lock_guard<std::mutex> lk(bp.mu);
+    if (bp.parked + b > cap) {
+        cudaFree(p);  // callers synchronised before releasing
+        return;
+    }
+    bp.free_list.emplace(std::make_pair(cur_device(), b), p);
+    bp.parked += b;
 }
+
+void kkt_release_pool() { pool_release_all(); }
 
 struct DevBuf {
     void* p = nullptr;

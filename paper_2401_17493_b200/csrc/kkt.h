@@ -29,5 +29,7 @@ void kkt_counters(KktCtx* k, long long out[3]);
 void kkt_set_counters(KktCtx* k, const long long in[3]);
 void kkt_get(KktCtx* k, int which, void* dst);
 void kkt_detgrad(KktCtx* k, double out[3]);
+// free every context buffer parked for reuse (all devices)
+void kkt_release_pool();
 
 }  // namespace frg

@@ -32,6 +32,11 @@ static void ensure_scratch() {
     }
 }
 
+// max / min that propagate NaN (np.max / np.min semantics; fmax / fmin drop
+// NaN operands, which would let a blown-up field report finite bounds)
+__device__ __forceinline__ double nmax(double a, double b) { return (a != a || b != b) ? a + b : fmax(a, b); }
+__device__ __forceinline__ double nmin(double a, double b) { return (a != a || b != b) ? a + b : fmin(a, b); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -39,12 +44,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = nmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = nmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
@@ -97,10 +102,10 @@ __global__ void __launch_bounds__(R_TPB) k_reduce_pass1(const TA* __restrict__ x
         if (OP == R_DOT) {
             a += xv * (double)y[i];
         } else if (OP == R_ABSMAX) {
-            a = fmax(a, fabs(xv));
+            a = nmax(a, fabs(xv));
         } else if (OP == R_MINMAXSUM) {
-            a = fmax(a, xv);
-            b = fmin(b, xv);
+            a = nmax(a, xv);
+            b = nmin(b, xv);
             c += xv;
         } else {
             a += isfinite(xv) ? 0.0 : 1.0;
@@ -123,10 +128,10 @@ __global__ void __launch_bounds__(R_TPB) k_reduce_pass2(const double* __restrict
         if (OP == R_DOT || OP == R_NONFINITE) {
             a += partials[i];
         } else if (OP == R_ABSMAX) {
-            a = fmax(a, partials[i]);
+            a = nmax(a, partials[i]);
         } else {
-            a = fmax(a, partials[i]);
-            b = fmin(b, partials[R_MAX_BLOCKS + i]);
+            a = nmax(a, partials[i]);
+            b = nmin(b, partials[R_MAX_BLOCKS + i]);
             c += partials[2 * R_MAX_BLOCKS + i];
         }
     }

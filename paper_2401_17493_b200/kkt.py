@@ -26,7 +26,7 @@ from .interp import check_method
 from .transport import Trajectory
 
 __all__ = ["RegConfig", "PrecondKind", "KktState", "evaluate_objective", "evaluate_gradient",
-           "hessian_matvec_gn", "apply_precond"]
+           "hessian_matvec_gn", "apply_precond", "release_device_pool"]
 
 
 @dataclass(frozen=True)
@@ -304,3 +304,11 @@ def hessian_matvec_gn(state: KktState, vtilde: VectorField) -> VectorField:
 
 def apply_precond(r: VectorField, kind: PrecondKind, state: KktState, outer_tol: float = 1e-6) -> VectorField:
     return state.apply_precond(r, kind, outer_tol)
+
+
+def release_device_pool() -> None:
+    """Free the device buffers destroyed contexts parked for reuse (the torch
+    caching allocator cannot reclaim them; call before large torch
+    allocations after a big solve)."""
+    torch.cuda.synchronize()
+    L.check(L.lib().frg_release_pool(), "release_pool")

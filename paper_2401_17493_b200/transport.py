@@ -87,6 +87,13 @@ class Trajectory:
         return self._points
 
 
+def _as(t: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    """The kernels read every operand in the series' dtype: convert mixed-dtype
+    operands (the reference accepts e.g. an f32 image with an f64 velocity)
+    instead of handing an f64 buffer to an f32 kernel."""
+    return t if t.dtype == dtype and t.is_contiguous() else t.to(dtype).contiguous()
+
+
 def _negated(v: VectorField) -> VectorField:
     return VectorField._wrap(v.grid, -v.data)
 
@@ -100,8 +107,9 @@ def solve_state(m0: ScalarField, v: VectorField, method: str = "cubic",
         trajectory = Trajectory.compute(v, method)
     out = torch.empty((grid.n_t + 1, *grid.n), dtype=m0.values.dtype, device="cuda")
     out[0] = m0.values
+    disp = _as(trajectory.disp, out.dtype)
     L.check(L.lib().frg_solve_state(L.n3(grid.n), grid.d, _dt(out), L.METHODS[method], grid.n_t,
-                                    L.ptr(trajectory.disp), L.ptr(out), L.stream()), "solve_state")
+                                    L.ptr(disp), L.ptr(out), L.stream()), "solve_state")
     return TimeSeriesField._wrap(grid, out)
 
 
@@ -116,8 +124,9 @@ def solve_adjoint(final: ScalarField, v: VectorField, method: str = "cubic", sch
         div_v = divergence(v, scheme=scheme)
     out = torch.empty((grid.n_t + 1, *grid.n), dtype=final.values.dtype, device="cuda")
     out[grid.n_t] = final.values
+    disp, dv = _as(back_trajectory.disp, out.dtype), _as(div_v.values, out.dtype)
     L.check(L.lib().frg_solve_adjoint(L.n3(grid.n), grid.d, _dt(out), L.METHODS[method], grid.n_t,
-                                      L.ptr(back_trajectory.disp), L.ptr(div_v.values), L.ptr(out), L.stream()),
+                                      L.ptr(disp), L.ptr(dv), L.ptr(out), L.stream()),
             "solve_adjoint")
     return TimeSeriesField._wrap(grid, out)
 
@@ -148,10 +157,11 @@ def solve_inc_state(mseries: TimeSeriesField, v: VectorField, vtilde: VectorFiel
         grad_slices = state_gradients(mseries, scheme)
     if len(grad_slices) != mseries.num_slices:
         raise ValueError("need one gradient slice per state slice")
-    grads = torch.stack([g.data for g in grad_slices]).contiguous()
     out = torch.empty((grid.n_t + 1, *grid.n), dtype=mseries.data.dtype, device="cuda")
+    grads = torch.stack([g.data for g in grad_slices]).to(out.dtype).contiguous()
+    disp = _as(trajectory.disp, out.dtype)
     L.check(L.lib().frg_solve_inc_state(L.n3(grid.n), grid.d, _dt(out), _dt(vtilde.data), L.METHODS[method],
-                                        grid.n_t, L.ptr(trajectory.disp), L.ptr(grads), L.ptr(vtilde.data),
+                                        grid.n_t, L.ptr(disp), L.ptr(grads), L.ptr(vtilde.data),
                                         L.ptr(out), L.stream()), "solve_inc_state")
     return TimeSeriesField._wrap(grid, out)
 
@@ -170,10 +180,11 @@ def solve_deformation_tensor(v: VectorField, method: str = "cubic", scheme: str 
     method = check_method(method)
     if trajectory is None:
         trajectory = Trajectory.compute(v, method)
-    jac = jacobian(v, scheme=scheme).contiguous()
     F = torch.empty((grid.d, grid.d, *grid.n), dtype=v.data.dtype, device="cuda")
+    jac = _as(jacobian(v, scheme=scheme), F.dtype)
+    disp = _as(trajectory.disp, F.dtype)
     L.check(L.lib().frg_deformation_tensor(L.n3(grid.n), grid.d, _dt(F), L.METHODS[method], grid.n_t,
-                                           L.ptr(trajectory.disp), L.ptr(jac), L.ptr(F), L.stream()),
+                                           L.ptr(disp), L.ptr(jac), L.ptr(F), L.stream()),
             "deformation_tensor")
     return TensorField._wrap(grid, F)
 

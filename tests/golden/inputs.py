@@ -72,7 +72,14 @@ def filter_inputs(shape, rng):
     return u, uc
 
 
-TRANSPORT_SHAPES = [(16, 12, 12), (16, 12)]
+# (12, 16, 64): every axis >= the fp32 TMA engine's box edge (csrc/sl_fast.cuh
+# tma_grid_ok), so the f32 transports run the TMA box + periodic patch path
+TRANSPORT_SHAPES = [(16, 12, 12), (16, 12), (12, 16, 64)]
+
+
+def transport_tag(shape):
+    """Fixture key prefix of a transport shape."""
+    return "3d_tma" if shape == (12, 16, 64) else f"{len(shape)}d"
 
 
 def transport_inputs(shape, rng):
@@ -94,14 +101,31 @@ KKT_CASES = [
     ("h1_none_ncc_cubic", (16, 12, 12), dict(order=1, incomp="none"), "ncc", "cubic", ("reg",)),
     ("h3f_near_ssd_cubic_2d", (24, 20), dict(order=3, seminorm=False, incomp="near-incompressible"),
      "ssd", "cubic", ("reg", "h0", "2level")),
+    # shapes on which the mixed / f32 contexts run the bench's engine: TMA
+    # boxes, per-map tile plans, periodic patches on every face (n0 = 12 is
+    # one box deep, so every tile wraps along axis 0)
+    ("tma_h1_near_ssd_cubic", (12, 16, 64), dict(order=1, incomp="near-incompressible"), "ssd", "cubic",
+     ("reg",)),
+    ("tma_h2_near_ssd_linear", (12, 16, 96), dict(order=2, incomp="near-incompressible"), "ssd", "linear",
+     ("reg",)),
+    # 20x the velocity: departure displacements of up to ~19 columns / 6 rows /
+    # 4 planes whose spread inside a tile overflows the fixed TMA box, so part
+    # of the tiles take the global-memory fallback (global_interp)
+    ("tma_wide_h1_none_ssd_cubic", (12, 16, 64), dict(order=1, incomp="none"), "ssd", "cubic", ("reg",)),
 ]
+KKT_VSCALE = {"tma_wide_h1_none_ssd_cubic": 20.0}
 
 
-def kkt_inputs(shape, rng):
+def kkt_case_inputs(case, rng):
+    """Inputs of one KKT_CASES entry (consumes ``rng`` in case order)."""
+    return kkt_inputs(case[1], rng, KKT_VSCALE.get(case[0], 1.0))
+
+
+def kkt_inputs(shape, rng, vscale=1.0):
     d = len(shape)
     m0 = bump(shape, rng.uniform(-1, 1, size=d)) + 0.2
     m1 = bump(shape, rng.uniform(-1, 1, size=d)) + 0.2
-    v = smooth_vector(rng, shape, 0.5, kmax=2)
+    v = smooth_vector(rng, shape, 0.5 * vscale, kmax=2)
     vt = smooth_vector(rng, shape, 1.0, kmax=3)
     r = smooth_vector(rng, shape, 1.0, kmax=4)
     return m0, m1, v, vt, r
@@ -115,4 +139,12 @@ REGISTER_CASES = [
     ("rot2d_h2_linear_h0", ("rotation", 64, 3, 2), dict(order=2, incomp="none"), "h0", "linear", True),
     ("rot3d_reg", ("rotation", 32, 1, 3), dict(order=1, incomp="none"), "reg", "cubic", True),
     ("c1_rot64_reg", ("rotation", 64, 1, 3), dict(order=1, incomp="none"), "reg", "cubic", False),
+]
+
+# BASELINE.json config C2: brain-like 128^3 (paper_2401_17493_b200.synth.
+# brain_arrays), H2 seminorm, linear interpolation, near-incompressible
+# (beta 1e-4), alpha 1e-3, spectral (reg) preconditioner.
+# name, (n, seed), reg kwargs, precond, method
+C2_CASES = [
+    ("c2_brain128_h2_linear", (128, 1), dict(order=2, incomp="near-incompressible", alpha=1e-3), "reg", "linear"),
 ]

@@ -34,3 +34,19 @@ with open(os.path.join(OUT, "dice.json"), "w") as fh:
                "empty_ids": list(res.empty_ids)}, fh, indent=1)
 write_dice_csv(os.path.join(OUT, "dice.csv"), {1: [0.5, 0.75, 0.9], 3: [0.25], 2: []})
 print("wrote", sorted(os.listdir(OUT)))
+
+# label transport + relative mismatch (metrics.py:90-129) on the 3D rotation
+# case: the reference's moved labels and its mismatch values
+from flowreg.metrics import relative_mismatch, transport_labels  # noqa: E402
+from flowreg.synth import synth_case  # noqa: E402
+
+m0, m1, vtrue = synth_case("rotation", 32, seed=1, d=3)
+lab = np.random.default_rng(3).integers(0, 4, size=(32, 32, 32)).astype(np.int32)
+moved = transport_labels(LabelVolume(vtrue.grid, lab), vtrue).labels
+np.savez_compressed(os.path.join(OUT, "labels_moved.npz"), moved=moved.astype(np.int8))
+half = VectorField(vtrue.grid, 0.5 * vtrue.data)
+mm = {d: list(relative_mismatch(m0, m1, half, distance=d)) for d in ("ssd", "ncc")}
+mm["zero"] = list(relative_mismatch(m0, m0, half))
+with open(os.path.join(OUT, "mismatch.json"), "w") as fh:
+    json.dump(mm, fh, indent=1)
+print("wrote labels_moved.npz / mismatch.json", mm)

@@ -89,7 +89,7 @@ def gen_transport():
     rng = np.random.default_rng(I.SEED + 2)
     out = {}
     for shape in I.TRANSPORT_SHAPES:
-        t = f"{len(shape)}d"
+        t = I.transport_tag(shape)
         g = Grid(shape, n_t=4)
         m0, v, vt, lam1 = I.transport_inputs(shape, rng)
         V = VectorField(g, v)
@@ -119,9 +119,10 @@ def make_reg(order=1, seminorm=True, incomp="none", alpha=1e-2, beta=1e-4):
 def gen_kkt():
     rng = np.random.default_rng(I.SEED + 3)
     out, meta = {}, {}
-    for name, shape, regkw, dist, method, preconds in I.KKT_CASES:
+    for case in I.KKT_CASES:
+        name, shape, regkw, dist, method, preconds = case
         g = Grid(shape, n_t=4)
-        m0, m1, v, vt, r = I.kkt_inputs(shape, rng)
+        m0, m1, v, vt, r = I.kkt_case_inputs(case, rng)
         st = kkt.KktState(ScalarField(g, m0), ScalarField(g, m1), make_reg(**regkw), distance=dist,
                           method=method, scheme="fd8", v_init=VectorField(g, v))
         p = name + "_"
@@ -172,8 +173,37 @@ def gen_synth():
         json.dump(meta, fh, indent=1)
 
 
+def gen_c2():
+    """BASELINE config C2: the brain-like 128^3 pair (inputs from the package's
+    pure-torch generator run on the CPU, m1 from the reference's own 64-step
+    cubic solve_state as synth.py:113-117 does), registered by the reference
+    at f64 with H2 / linear / near-incompressible / reg preconditioner."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2401_17493_b200.synth import brain_arrays
+
+    meta, out = {}, {}
+    for name, (n, seed), regkw, pre, method in I.C2_CASES:
+        vals, vtrue = brain_arrays(n, seed, 3, device="cpu")
+        vals, vtrue = vals.numpy(), vtrue.numpy()
+        g = Grid((n,) * 3, n_t=4)
+        fine = g.with_time_steps(64)
+        m1 = transport.solve_state(ScalarField(fine, vals), VectorField(fine, vtrue), method="cubic").final().values
+        v, rep = optimizer.register(ScalarField(g, vals), ScalarField(g, m1), reg=make_reg(**regkw),
+                                    precond=kkt.PrecondKind(pre), method=method, scheme="fd8")
+        r = rep.to_dict()
+        r.pop("runtime")
+        r["m0_sum"], r["m1_sum"], r["m1_sumsq"] = float(vals.sum()), float(m1.sum()), float((m1 * m1).sum())
+        meta[name] = r
+        out[name + "_m1_sub"] = m1[::4, ::4, ::4].copy()
+        out[name + "_v_sub"] = v.data[:, ::4, ::4, ::4].astype(np.float32)
+        print(name, r["iterations"], r["matvecs"], r["pde_solves"], r["status"], flush=True)
+    save("c2.npz", out)
+    with open(os.path.join(OUT, "c2.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 def main():
-    which = sys.argv[1:] or ["sample", "diffops", "transport", "kkt", "synth", "register"]
+    which = sys.argv[1:] or ["sample", "diffops", "transport", "kkt", "synth", "register", "c2"]
     for w in which:
         globals()["gen_" + w]()
 

@@ -151,7 +151,7 @@ def test_transport_matches_reference(golden, shape, method, dtype):
         m0, v, vt, lam1 = I.transport_inputs(s, rng)
         if s == shape:
             break
-    k = f"{len(shape)}d_{method}"
+    k = f"{I.transport_tag(shape)}_{method}"
     grid = Grid(shape, n_t=4, dtype=dtype)
     V = VectorField(grid, v)
 
@@ -200,7 +200,7 @@ def _reg(regkw):
 def _kkt_case(name):
     rng = np.random.default_rng(I.SEED + 3)
     for c in I.KKT_CASES:
-        ins = I.kkt_inputs(c[1], rng)
+        ins = I.kkt_case_inputs(c, rng)
         if c[0] == name:
             return c, ins
     raise KeyError(name)
@@ -292,21 +292,128 @@ def test_nonfinite_and_grid_errors():
 # ---------------------------------------------------------------------------
 # a16, a18: optimizer / continuation end to end
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name", [c[0] for c in I.REGISTER_CASES if c[5]])
-def test_register_matches_reference(golden, name):
+_REG_PARAMS = [(c[0], "f64") for c in I.REGISTER_CASES] + [("c1_rot64_reg", "mixed")]
+
+
+@pytest.mark.parametrize("name,mode", _REG_PARAMS, ids=[f"{a}-{b}" for a, b in _REG_PARAMS])
+def test_register_matches_reference(golden, name, mode):
+    """Every REGISTER_CASES golden, including BASELINE config C1 (64^3 rotation,
+    H1, reg preconditioner: the reference runs 4 Newton iterations / 15 matvecs
+    / 44 PDE solves) — f64 and, for C1, the mixed (bench) precision."""
     meta = golden("register.json")[name]
-    gv = golden("register.npz")[name + "_v"]
     case = next(c for c in I.REGISTER_CASES if c[0] == name)
-    _, (sc, n, seed, d), regkw, pre, method, _ = case
+    _, (sc, n, seed, d), regkw, pre, method, store_v = case
     m0, m1, _ = F.synth_case(sc, n, seed=seed, d=d)
-    v, rep = F.register(m0, m1, reg=_reg(regkw), precond=PrecondKind(pre), method=method, scheme="fd8")
+    tdt = np.float32 if mode == "mixed" else None
+    v, rep = F.register(m0, m1, reg=_reg(regkw), precond=PrecondKind(pre), method=method, scheme="fd8",
+                        transport_dtype=tdt)
     assert rep.status == meta["status"]
     assert rep.exit_reason == meta["exit_reason"]
     assert rep.iterations == meta["iterations"]
     assert rep.matvecs == meta["matvecs"]
     assert rep.pde_solves == meta["pde_solves"]
     assert rep.line_search_evals == meta["line_search_evals"]
+    assert rep.precond_fallbacks == meta["precond_fallbacks"]
     assert [t["pcg_iterations"] for t in rep.trace] == [t["pcg_iterations"] for t in meta["trace"]]
-    assert rep.mismatch == pytest.approx(meta["mismatch"], rel=1e-6)
-    assert rep.detgrad_min == pytest.approx(meta["detgrad_min"], rel=1e-6)
-    assert rel_l2(np_(v), gv) < 1e-5
+    rt = 1e-6 if mode == "f64" else 1e-5
+    assert rep.mismatch == pytest.approx(meta["mismatch"], rel=rt)
+    assert rep.gradient == pytest.approx(meta["gradient"], rel=1e-4 if mode == "f64" else 1e-3)
+    assert rep.detgrad_min == pytest.approx(meta["detgrad_min"], rel=rt)
+    assert rep.detgrad_max == pytest.approx(meta["detgrad_max"], rel=rt)
+    for a, b in zip(rep.trace, meta["trace"]):
+        assert a["objective"] == pytest.approx(b["objective"], rel=rt)
+    if store_v:
+        assert rel_l2(np_(v), golden("register.npz")[name + "_v"]) < 1e-5
+
+
+def test_tma_golden_shapes_exercise_fast_engine():
+    """The TMA-sized golden cases really run the bench's engine: every axis is
+    >= the box edge, and the 'wide' case has tiles whose stencil bounding box
+    overflows the fixed 12 x 16 x 64 box (global-memory fallback) next to
+    tiles that fit (the same plan rule as k_tile_plan, csrc/sl_fast.cuh)."""
+    from oracle import flowreg_oracle as O
+
+    rng = np.random.default_rng(I.SEED + 3)
+    counts = {}
+    for c in I.KKT_CASES:
+        m0, m1, v, vt, r = I.kkt_case_inputs(c, rng)
+        if not c[0].startswith("tma_"):
+            continue
+        n = c[1]
+        assert n[0] >= 12 and n[1] >= 16 and n[2] >= 64 and n[2] % 4 == 0
+        y = O.departure(v, 1.0 / 4, c[4])
+        b = [np.floor(qa).astype(np.int64).reshape(n) for qa in O.frac_index(n, y)]
+        lo, hi = (1, 2) if c[4] == "cubic" else (0, 1)
+        fit = over = 0
+        for i0 in range(0, n[0], 4):
+            for j0 in range(0, n[1], 8):
+                for k0 in range(0, n[2], 32):
+                    sl = (slice(i0, i0 + 4), slice(j0, j0 + 8), slice(k0, k0 + 32))
+                    mn = [int(b[a][sl].min()) - lo for a in range(3)]
+                    mx = [int(b[a][sl].max()) + hi for a in range(3)]
+                    mn[2] &= ~3
+                    s = [mx[a] - mn[a] + 1 for a in range(3)]
+                    if s[0] <= 12 and s[1] <= 16 and s[2] <= 64:
+                        fit += 1
+                    else:
+                        over += 1
+        counts[c[0]] = (fit, over)
+    assert counts["tma_wide_h1_none_ssd_cubic"][0] > 0 and counts["tma_wide_h1_none_ssd_cubic"][1] > 0, counts
+    assert counts["tma_h1_near_ssd_cubic"][0] > 0, counts
+
+
+def test_reductions_propagate_nan():
+    """np.max / np.min semantics: a partly-NaN field reports NaN
+    bounds instead of the max / min of its finite part."""
+    import math
+
+    from paper_2401_17493_b200 import _lib as L
+
+    x = torch.zeros((3, 16, 16, 16), dtype=torch.float64, device="cuda")
+    x[1, 3, 4, 5] = float("nan")
+    x[2, 0, 0, 0] = 7.0
+    assert math.isnan(F.norm_inf(VectorField._wrap(Grid((16, 16, 16)), x)))
+    for dt in (torch.float64, torch.float32):
+        y = x.to(dt)
+        mms = (L.ctypes.c_double * 3)()
+        L.check(L.lib().frg_min_max_sum(L.dtype_code(y.dtype), L.ptr(y), y.numel(), mms, L.stream()), "mms")
+        assert math.isnan(mms[0]) and math.isnan(mms[1]) and math.isnan(mms[2])
+    y = torch.zeros_like(x)
+    y[2, 0, 0, 0] = -7.0
+    assert F.norm_inf(VectorField._wrap(Grid((16, 16, 16)), y)) == 7.0
+
+
+def test_mixed_dtype_transport_operands():
+    """An f32 image transported by an f64 velocity / trajectory (accepted by the
+    reference) equals the all-f32 transport (the f64 displacement
+    buffer must not be read as f32 bits)."""
+    rng = np.random.default_rng(11)
+    shape = (16, 12, 12)
+    m0, v, vt, lam1 = I.transport_inputs(shape, rng)
+    g64, g32 = Grid(shape, n_t=4), Grid(shape, n_t=4, dtype=np.float32)
+    V64, V32 = VectorField(g64, v), VectorField(g32, v)
+    traj64 = transport.Trajectory.compute(V64, "cubic")
+    ref = np_(transport.solve_state(ScalarField(g32, m0), V32, "cubic"))
+    got = np_(transport.solve_state(ScalarField(g32, m0), V64, "cubic", traj64))
+    assert rel_l2(got, ref) < 1e-6
+    ref_a = np_(transport.solve_adjoint(ScalarField(g32, lam1), V32, "cubic"))
+    got_a = np_(transport.solve_adjoint(ScalarField(g32, lam1), V64, "cubic", "fd8",
+                                        transport.Trajectory.compute(VectorField(g64, -v), "cubic"),
+                                        diffops.divergence(V64, "fd8")))
+    assert rel_l2(got_a, ref_a) < 1e-6
+
+
+def test_release_device_pool():
+    """Buffers parked by destroyed contexts go back to the device on request."""
+    import gc
+
+    m0, m1, _ = F.synth_case("rotation", 64, seed=1, d=3)
+    st = KktState(m0, m1, _reg({}), transport_dtype=np.float32)
+    st.gradient()
+    del st
+    gc.collect()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    F.release_device_pool()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free1 > free0

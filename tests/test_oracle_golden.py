@@ -88,7 +88,7 @@ def test_transport_matches_reference(golden, shape, method):
         m0, v, vt, lam1 = I.transport_inputs(s, rng)
         if s == shape:
             break
-    k = f"{len(shape)}d_{method}"
+    k = f"{I.transport_tag(shape)}_{method}"
     n_t = 4
     y = O.departure(v, 1.0 / n_t, method)
     yb = O.departure(-v, 1.0 / n_t, method)
@@ -117,7 +117,7 @@ def test_kkt_matches_reference(golden, case):
     meta = golden("kkt.json")
     rng = np.random.default_rng(I.SEED + 3)
     for c in I.KKT_CASES:
-        ins = I.kkt_inputs(c[1], rng)
+        ins = I.kkt_case_inputs(c, rng)
         if c[0] == case[0]:
             break
     name, shape, regkw, dist, method, preconds = case
