@@ -40,6 +40,9 @@ namespace frg {
 #ifndef FRG_SLF_MINB_MF
 #define FRG_SLF_MINB_MF 3  // the same for multi-field gathers (single box)
 #endif
+#ifndef FRG_SLF_MINB_DB
+#define FRG_SLF_MINB_DB 2  // the same for double-buffered multi-field gathers (FRG_SL_DB)
+#endif
 #ifndef FRG_SLF_MINB
 #define FRG_SLF_MINB 4  // resident CTAs per SM the single-field engine is register-budgeted for
 #endif
@@ -363,7 +366,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 }
 
 template <int M, int NF, class Op>
-__global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? 2 : FRG_SLF_MINB_MF))
+__global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
     k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");

@@ -13,6 +13,8 @@
 #include <tuple>
 
 #include "ops.h"
+#include <cstdlib>
+
 #include "spectral.h"
 
 #include <type_traits>
@@ -935,6 +937,8 @@ void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a
 }
 
 void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st) {
+    if (in != out && bspline_fir_applies(g, dtype) && !getenv("FRG_BSPLINE_SPECTRAL"))
+        return bspline_prefilter_fir(g, dtype, in, out, st);
     RegSpec r{1.0, 1, 1, 0, 1e-4};
     spectral_apply(g, dtype, 1, in, out, SK_BSPLINE_PREFILTER, r, st);
 }

@@ -50,4 +50,9 @@ double reg_energy_ex(PlanCache& pc, void* ws, const Dims& g, int dtype, const vo
 void restrict_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
 void prolong_field_ex(PlanCache& pc, void* ws, const Dims& gf, int dtype, const void* in, void* out, cudaStream_t st);
 
+// B-spline prefilter as separable FIR passes (bspline.cu): applies to whole
+// grids whose axes are all 1 or >= 2K + 2 long (K = 16 fp32, 32 f64)
+bool bspline_fir_applies(const Dims& g, int dtype);
+void bspline_prefilter_fir(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st);
+
 }  // namespace frg

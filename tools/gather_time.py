@@ -49,4 +49,6 @@ def timeit(fn, reps):
 gat = timeit(lambda: L.check(L.lib().frg_gather_planned(nn, 3, 2, ctypes.c_void_p(disp.data_ptr()), L.ptr(plan), 1,
                                                         ins, outs, L.stream()), "gather"), 30)
 mv = timeit(lambda: st.hessian_matvec(vt, out=out), 20)
-print(f"{os.environ.get('FRG_LIB', 'default')}: gather {gat:.1f} us  matvec {mv:.1f} us")
+vv = F.VectorField._wrap(m0.grid, 0.5 * vtrue.data)
+rf = timeit(lambda: st.refresh(vv), 10)
+print(f"{os.environ.get('FRG_LIB', 'default')}: gather {gat:.1f} us  matvec {mv:.1f} us  refresh {rf:.1f} us")

@@ -24,6 +24,7 @@ ap.add_argument("--what", default="matvec", choices=["matvec", "refresh", "gathe
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--precision", default="mixed")
 ap.add_argument("--interp", default="fp32", choices=["fp32", "fp16"])
+ap.add_argument("--method", default="cubic", choices=["cubic", "linear", "bspline"])
 a = ap.parse_args()
 
 n = a.n
@@ -33,7 +34,7 @@ m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3, dtype=dtype)
 grid = m0.grid
 reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
 v = F.VectorField._wrap(grid, 0.5 * vtrue.data)
-st = F.KktState(m0, m1, reg, v_init=v, transport_dtype=tdt, interp_precision=a.interp)
+st = F.KktState(m0, m1, reg, method=a.method, v_init=v, transport_dtype=tdt, interp_precision=a.interp)
 gen = torch.Generator(device="cuda").manual_seed(0)
 vt = F.VectorField._wrap(grid, 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=grid.torch_dtype, device="cuda"))
 out = torch.empty_like(vt.data)
