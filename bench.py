@@ -12,9 +12,14 @@ vectors in fp64 (SURVEY.md §7 hard part 1).  Synthetic data generated on the
 device.  Every matvec touches several GB, far above the 126 MB L2, so no L2
 flush is needed between steps.
 
-Multi-GPU (torchrun, one rank per GPU): every rank solves its own 256^3
-problem (independent registrations, weak scaling, no data-path collective);
-the barrier + max-over-ranks timing uses NCCL.
+Multi-GPU (torchrun, one rank per GPU): the headline is ONE slab-decomposed
+problem (dist.py) — config C4, 512^3 at N = 2 / 4, config C5's 1024^3 at
+N = 8 (``--slab-n`` overrides) — generated slab by slab on the ranks
+(dist.slab_synth), GN Hessian matvecs/s of that problem (strong scaling,
+NCCL all-to-all FFT transposes + ghost-plane exchanges), its time to
+solution (SPMD dist_register) and its e2e rate with host buffers.  A slab
+failure exits non-zero.  ``--slab`` runs the same path at N = 1 (P = 1).
+The barrier + max-over-ranks timing uses NCCL.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port, oracle/flowreg_oracle.py: C/OpenMP gathers + pocketfft) on the
@@ -48,8 +53,9 @@ def parse():
     ap.add_argument("--precision", default="mixed", choices=["mixed", "f64", "f32"])
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--no-slab", action="store_true", help="skip the multi-GPU slab-decomposed C4 run (N > 1)")
-    ap.add_argument("--slab-n", type=int, default=512, help="grid of the slab-decomposed run (N > 1)")
+    ap.add_argument("--slab", action="store_true", help="slab-decomposed headline at N = 1 too (P = 1)")
+    ap.add_argument("--slab-n", type=int, default=0,
+                    help="grid of the slab-decomposed headline (default 512, 1024 at N = 8)")
     return ap.parse_args()
 
 
@@ -155,6 +161,9 @@ def run_b200(a):
 
     import paper_2401_17493_b200 as F
     from paper_2401_17493_b200 import _lib as L
+
+    if world > 1 or a.slab:
+        return run_slab(a, F, L, world, rank, local, backend)
 
     n = a.n
     dtype = np.float32 if a.precision == "f32" else np.float64
@@ -358,13 +367,6 @@ def run_b200(a):
                           "matvec_per_s": reps / (c0_.elapsed_time(c1_) / 1e3)})
             del s2
 
-    slab = None
-    if world > 1 and not a.no_slab:
-        try:
-            slab = run_slab(a, F, world, rank, barrier, max_over_ranks)
-        except Exception as exc:  # keep the headline line even if the slab run fails
-            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-
     if world > 1:
         dist.barrier()
     result = None
@@ -375,7 +377,7 @@ def run_b200(a):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 transport / f64 control" if a.precision == "mixed" else a.precision,
             "data": "synthetic (synth_case rotation, generated on device)",
-            "config": dict(config(n, a.precision), parallelism=f"independent 256^3 problem per rank x{world}"),
+            "config": dict(config(n, a.precision), parallelism="single GPU"),
             "e2e": e2e, "gpu_launches": gpu_launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> (one TMA-staged SL gather step with its tile plan, frg_gather_planned)",
@@ -385,8 +387,6 @@ def run_b200(a):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        if slab is not None:
-            result["slab"] = slab
         if other:
             result["other_configs"] = other
         print(json.dumps(result))
@@ -396,55 +396,167 @@ def run_b200(a):
     return result
 
 
-def run_slab(a, F, world, rank, barrier, max_over_ranks):
-    """C4: ONE slab-decomposed registration problem across the N ranks
-    (dist.py: NCCL all-to-all FFT transposes + ghost-plane exchanges), GN
-    Hessian matvecs/s of that single problem (strong scaling)."""
+def run_slab(a, F, L, world, rank, local, backend):
+    """C4 / C5 headline: ONE slab-decomposed registration problem over the N
+    ranks (dist.py: all-to-all FFT transposes + ghost-plane exchanges)."""
+    import ctypes
+
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     from paper_2401_17493_b200 import dist as D
 
-    n = a.slab_n
-    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29571")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    n = a.slab_n or (1024 if world >= 8 else 512)
+    comm = D.SlabComm()
+    staged = comm.staged
+
+    def barrier():
+        dist.barrier()
+
+    def max_over_ranks(x):
+        return comm.all_reduce(x, "max")
+
+    m0, m1, vtrue = D.slab_synth("rotation", n, comm)
     reg = F.RegConfig(alpha=1e-2, operator=F.RegOperatorSpec(1, True),
                       incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
-    comm = D.SlabComm()
-    lo, hi = D.slab_bounds(n, world, rank)
-    v = (0.5 * vtrue.data[:, lo:hi]).contiguous()
-    st = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n), v_init=v)
-    del m0, m1, vtrue
+    v = (0.5 * vtrue).contiguous()
+    st = D.DistKktState(m0, m1, reg, comm, (n, n, n), v_init=v)
     gen = torch.Generator(device="cuda").manual_seed(rank)
-    vt = 0.1 * torch.randn((3, hi - lo, n, n), generator=gen, dtype=torch.float64, device="cuda")
+    n0l = n // world
+    vt = 0.1 * torch.randn((3, n0l, n, n), generator=gen, dtype=torch.float64, device="cuda")
     out = torch.empty_like(vt)
-    steps = max(3, min(a.steps, 10))
+    stream = torch.cuda.current_stream()
     for _ in range(max(a.warmup, 3)):
         st.hessian_matvec(vt, out=out)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     b0 = comm.bytes_sent
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record()
-    for _ in range(steps):
-        st.hessian_matvec(vt, out=out)
-    s1.record()
+    c0 = st.matvecs
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            st.hessian_matvec(vt, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    assert st.matvecs - c0 == a.steps
+    t = max_over_ranks(e0.elapsed_time(e1)) / 1e3
+    ms = 1e3 * t / a.steps
+    value = a.steps / t
+    sent = (comm.bytes_sent - b0) / a.steps  # payload each rank sent per matvec (halo + all-to-all chunks)
+    peak, peak_src = peaks()
+    canon = 174 * 4 * n ** 3 / world
+
+    # dominant kernel: one planned single-field SL gather step on this rank's slab
+    src = torch.randn((1, n0l, n, n), generator=gen, dtype=torch.float32, device="cuda")
+    ext = st._ext(src, st.Wf)
+    g_out = torch.empty((n0l, n, n), dtype=torch.float32, device="cuda")
+    st._bind()
+    for _ in range(3):
+        st._gather(st.disp_f, st.Wf, [ext[0]], [g_out])
+    torch.cuda.synchronize()
+    reps = 20
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(reps):
+        st._gather(st.disp_f, st.Wf, [ext[0]], [g_out])
+    g1.record(stream)
+    torch.cuda.synchronize()
+    t_gather = g0.elapsed_time(g1) / reps / 1e3
+    alg_bytes = n0l * n * n * 20
+
+    # e2e: this rank's v~ slab from pinned host, the matvec, the result back, every step
+    host_in = torch.empty(vt.shape, dtype=vt.dtype).pin_memory()
+    host_in.copy_(vt)
+    host_out = torch.empty_like(host_in).pin_memory()
+    dev_in = torch.empty_like(vt)
+    e2e_steps = max(3, min(a.steps, 10))
+    barrier()
+    torch.cuda.synchronize()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for _ in range(e2e_steps):
+        dev_in.copy_(host_in, non_blocking=True)
+        st.hessian_matvec(dev_in, out=out)
+        host_out.copy_(out, non_blocking=True)
+    x1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    t = max_over_ranks(s0.elapsed_time(s1)) / 1e3
-    sent = (comm.bytes_sent - b0) / steps  # NVLink payload per matvec per rank (halo + all-to-all)
-    canon = 174 * 4 * n ** 3 / world       # SURVEY 8d canonical HBM bytes per matvec per rank
-    peak, _ = peaks()
-    return {"workload": f"C4: one {n}^3 GN Hessian matvec slab-decomposed over {world} ranks", "grid": [n] * 3,
-            "ranks": world, "value": steps / t, "unit": UNIT, "ms_per_step": 1e3 * t / steps, "steps": steps,
-            "scaling": "strong", "halo_planes": [st.Wf, st.Wb],
-            "nvlink_bytes_per_step_per_rank": sent,
-            "nvlink_roofline": {"achieved_gbs": sent / (t / steps) / 1e9, "peak_gbs": 900.0,
-                                "frac": sent / (t / steps) / 900e9, "note": "payload sent per rank / step time"},
-            "hbm_roofline": {"achieved_gbs": canon / (t / steps) / 1e9, "peak_gbs": peak,
-                             "frac": canon / (t / steps) / 1e9 / peak,
-                             "note": "SURVEY 8d canonical 174 fp32 field passes per matvec, per rank"},
-            "parallelism": f"slab along axis 0 x{world}: NCCL all-to-all FFT transposes, ghost-plane send/recv"}
+    t_e2e = max_over_ranks(x0.elapsed_time(x1)) / 1e3
+
+    # time to solution of the same problem: SPMD dist_register (reg preconditioner)
+    tts = None
+    halo = [st.Wf, st.Wb]
+    if not a.no_tts:
+        del st
+        torch.cuda.synchronize()
+        barrier()
+        walls = []
+        for _ in range(2):  # the first solve creates the cuFFT plans
+            torch.cuda.synchronize()
+            barrier()
+            w0 = time.perf_counter()
+            _, rep = D.dist_register(m0, m1, comm, (n, n, n), reg=reg)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - w0)
+        tts = {"seconds": max_over_ranks(walls[-1]), "first_call_seconds": max_over_ranks(walls[0]),
+               "iterations": rep.iterations, "matvecs": rep.matvecs, "pde_solves": rep.pde_solves,
+               "status": rep.status, "mismatch": rep.mismatch, "precond": "reg", "detgrad_min": rep.detgrad_min,
+               "includes": "DistKktState creation, all refresh/gradient/PCG/Armijo work and det(F) stats over the "
+                           "slabs; excludes synthetic-data generation"}
+
+    # launches of our kernels per slab matvec: 3 converts, IncFirst, n_t-1 IncStep, n_t adjoint steps, body
+    # force, 2D/1D spectra (2 forward + 1 inverse: 3 x (fft2 + fft1) are cuFFT, not counted), transposes
+    # (4 at P > 1), combine, widening convert
+    launches = 3 + 1 + 3 + 4 + 1 + (4 if world > 1 else 0) + 1 + 1
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 transport / f64 control", "data": "synthetic (dist.slab_synth rotation, generated slab by "
+                                                            "slab on the ranks, fp32 64-step reference transport)",
+            "config": {"workload": f"{'C5' if n >= 1024 else 'C4'}: ONE {n}^3 GN Hessian matvec slab-decomposed "
+                                   f"over {world} rank(s), nt=4, cubic-Lagrange SL, FD8, H1 alpha=1e-2, "
+                                   "near-incompressible beta=1e-4, SSD",
+                       "grid": [n, n, n], "n_t": 4, "interp": "cubic", "precision": "mixed",
+                       "parallelism": f"slab along axis 0 x{world} ({'gloo-staged' if staged else 'NCCL'} "
+                                      "all-to-all FFT transposes, ghost-plane send/recv)",
+                       "halo_planes": halo,
+                       "l2": "inputs > L2 (GB-scale working set per matvec, no flush needed)"},
+            "e2e": {"value": e2e_steps / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": host_in.numel() * host_in.element_size() * world,
+                    "d2h_bytes_per_step": host_out.numel() * host_out.element_size() * world,
+                    "steps": e2e_steps, "path": "pinned host v~ slab per rank -> DistKktState.hessian_matvec -> "
+                                                "pinned host, serial per step"},
+            "gpu_launches": launches * a.steps,
+            "roofline": {"bound": "hbm", "achieved": alg_bytes / t_gather / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg_bytes / t_gather / 1e9 / peak, "traffic": None,
+                         "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> on this rank's slab (frg_slab_gather, tile plan, "
+                                   "ghost planes)", "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather,
+                         "peak_source": peak_src},
+            "matvec_roofline": {"canonical_bytes_per_rank": canon, "achieved_gbs": canon / (t / a.steps) / 1e9,
+                                "peak_gbs": peak, "frac": canon / (t / a.steps) / 1e9 / peak,
+                                "note": "SURVEY.md §8d canonical 174 fp32 field passes per matvec, per rank"},
+            "nvlink": {"bytes_per_step_per_rank": sent, "achieved_gbs": sent / (t / a.steps) / 1e9,
+                       "peak_gbs": 900.0, "frac": sent / (t / a.steps) / 900e9,
+                       "note": "payload each rank sends per matvec (halo planes + off-rank all-to-all chunks) / "
+                               "step time; 0 at P = 1"},
+            "time_to_solution": tts,
+            "clocks": clk.summary(),
+            "cpu_baseline": None,
+        }
+        print(json.dumps(res))
+    barrier()
+    dist.destroy_process_group()
+    return None
 
 
 def cpu_baseline(a, m0, m1, vtrue, vt):

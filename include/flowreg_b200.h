@@ -234,8 +234,9 @@ int frg_slab_adjoint_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, i
 int frg_slab_inc_first(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, int32_t n_t,
                        const void* disp, const void* grads, const void* grads_y, const void* vt_src,
                        const void* vt_loc, void* m1, void* S, void* stream);
+/* fin (optional, owned planes): fin = fsign * m_next (SSD: lam~(1) = -m~(1)) */
 int frg_slab_inc_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
-                      const void* m_src, const void* S_j, void* m_next, void* stream);
+                      const void* m_src, const void* S_j, void* m_next, void* fin, double fsign, void* stream);
 int frg_slab_fd8_gradient(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t nslices, const void* u_src,
                           void* out, void* stream);
 int frg_slab_fd8_divergence(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, const void* v_src, void* out,
@@ -253,6 +254,17 @@ int frg_slab_transpose(int32_t dir, int32_t nranks, const int32_t n_loc[3], int3
 /* symbol (FRG_SYM_*) / N on the split spectrum of rows [i1_off, i1_off + n1_loc) */
 int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, int32_t ncomp,
                         void* x, int32_t kind, const frg_reg* reg, void* stream);
+/* mixed precision (the single-GPU mixed path's arithmetic): a = f64 spectrum
+ * of alpha L's argument (NULL: P(b) only), b = f32 spectrum, in / out:
+ * b = alpha L a + P(b) (normalised) */
+int frg_slab_spec_combine_mixed(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, const void* a, void* b,
+                                const frg_reg* reg, int32_t project, void* stream);
+/* sum_x |grad x|^2 (spectral gradient, Nyquist-zeroed) from this rank's share
+ * of the f64 split spectrum of x: the local part, all-reduce to complete */
+int frg_slab_grad_energy(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, const void* x_spec, double* out,
+                         void* stream);
+/* dst = (ddtype) src, f32 <-> f64 (vectorised) */
+int frg_convert(int32_t sdtype, const void* src, int32_t ddtype, void* dst, int64_t n, void* stream);
 /* a = alpha L a + P(b) (normalised); a == b: P(b) only */
 int frg_slab_spec_combine(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, int32_t dtype, void* a,
                           const void* b, const frg_reg* reg, int32_t project, void* stream);

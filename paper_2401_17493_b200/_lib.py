@@ -108,7 +108,10 @@ PROTOTYPES = {
     "frg_slab_adjoint_multiplier": [_N3, _I, _I, _I, _D, _P, _P, _P, _P, _P],
     "frg_slab_adjoint_step": [_N3, _I, _I, _I, _P, _P, _P, _P, _P],
     "frg_slab_inc_first": [_N3, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
-    "frg_slab_inc_step": [_N3, _I, _I, _I, _P, _P, _P, _P, _P],
+    "frg_slab_inc_step": [_N3, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.c_double, _P],
+    "frg_slab_spec_combine_mixed": [_N3, _I, _I, _P, _P, ctypes.POINTER(FrgReg), _I, _P],
+    "frg_slab_grad_energy": [_N3, _I, _I, _P, _DP, _P],
+    "frg_convert": [_I, _P, _I, _P, _L, _P],
     "frg_slab_fd8_gradient": [_N3, _I, _I, _I, _P, _P, _P],
     "frg_slab_fd8_divergence": [_N3, _I, _I, _P, _P, _P],
     "frg_slab_fft2": [_N3, _I, _I, _I, _P, _P, _P],

@@ -567,11 +567,11 @@ int frg_slab_inc_first(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int3
 }
 
 int frg_slab_inc_step(const int32_t n_loc[3], int32_t n0_glob, int32_t h0, int32_t method, const void* disp,
-                      const void* m_src, const void* S_j, void* m_next, void* stream) {
+                      const void* m_src, const void* S_j, void* m_next, void* fin, double fsign, void* stream) {
     return guard([&] {
         check_slab_method(method);
         inc_step(slab_dims(n_loc, n0_glob, h0), method, (const float*)disp, (const float*)m_src, (const float*)S_j,
-                 (float*)m_next, ST(stream));
+                 (float*)m_next, ST(stream), (float*)fin, (float)fsign);
     });
 }
 
@@ -621,6 +621,27 @@ int frg_slab_spec_apply(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc,
         check_dtype(dtype);
         FRG_REQUIRE(kind >= 0 && kind <= 7, "unknown symbol kind");
         slab_spec_scale(dims_of(n_glob, 3), i1_off, n1_loc, dtype, ncomp, x, kind, reg_of(reg), ST(stream));
+    });
+}
+
+int frg_slab_spec_combine_mixed(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, const void* a, void* b,
+                                const frg_reg* reg, int32_t project, void* stream) {
+    return guard([&] {
+        FRG_REQUIRE(b != nullptr, "slab_spec_combine_mixed: b spectrum required");
+        slab_spec_combine_mixed(dims_of(n_glob, 3), i1_off, n1_loc, a, b, reg_of(reg), project != 0, ST(stream));
+    });
+}
+
+int frg_slab_grad_energy(const int32_t n_glob[3], int32_t i1_off, int32_t n1_loc, const void* x_spec, double* out,
+                         void* stream) {
+    return guard([&] { *out = slab_grad_energy(dims_of(n_glob, 3), i1_off, n1_loc, x_spec, ST(stream)); });
+}
+
+int frg_convert(int32_t sdtype, const void* src, int32_t ddtype, void* dst, int64_t n, void* stream) {
+    return guard([&] {
+        check_dtype(sdtype);
+        check_dtype(ddtype);
+        convert(sdtype, src, ddtype, dst, n, ST(stream));
     });
 }
 

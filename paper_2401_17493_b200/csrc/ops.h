@@ -36,7 +36,7 @@ void adjoint_multiplier(const Dims& g, int tdtype, int method, double h_t, const
 void inc_first(const Dims& g, int method, int n_t, const float* disp, const float* grads, const float* grads_y,
                const float* vt_src, const float* vt_loc, float* m1, float* S, cudaStream_t st);
 void inc_step(const Dims& g, int method, const float* disp, const float* m_src, const float* Sj, float* m_next,
-              cudaStream_t st);
+              cudaStream_t st, float* fin = nullptr, float fsign = 0.f);
 // one backward step: out = u(y_b) * c
 void adjoint_step(const Dims& g, int tdtype, int method, const void* disp_b, const void* cmul,
                   const void* u, void* out, cudaStream_t st);
@@ -145,6 +145,13 @@ void slab_transpose(int dir, int P, int n0_loc, int n1, int nh, int elem_bytes, 
 void slab_spec_scale(const Dims& g, int i1_off, int n1_loc, int dtype, int ncomp, void* x, int kind,
                      const RegSpec& r, cudaStream_t st);
 // a = alpha L a + P(b) (normalised); a == b: P(b) only
+// mixed precision: a (f64 spectrum, or nullptr: P(b) only), b (f32 spectrum)
+// in / out: b = alpha L a + P(b) in fp32 arithmetic per bin
+void slab_spec_combine_mixed(const Dims& g, int i1_off, int n1_loc, const void* a, void* b, const RegSpec& r,
+                             bool project, cudaStream_t st);
+// sum over the split spectrum of |grad|^2 weights (Nyquist-zeroed integer
+// wavenumbers) x |x_k|^2, half-spectrum bins doubled, / N (= sum_x |grad x|^2)
+double slab_grad_energy(const Dims& g, int i1_off, int n1_loc, const void* x_spec, cudaStream_t st);
 void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a, const void* b, const RegSpec& r,
                        bool project, cudaStream_t st);
 

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "ops.h"
 #include <cstdlib>
@@ -934,6 +935,59 @@ void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a
                                                                      (const cufftComplex*)b, (cufftComplex*)a, r,
                                                                      invN, a != b, project);
     FRG_CHECK_LAUNCH();
+}
+
+void slab_spec_combine_mixed(const Dims& g, int i1_off, int n1_loc, const void* a, void* b, const RegSpec& r,
+                             bool project, cudaStream_t st) {
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    const double invN = 1.0 / ((double)g.n0 * g.n1 * g.n2);
+    k_slab_combine<cufftDoubleComplex, cufftComplex, cufftComplex><<<slab_blocks(cnt), 256, 0, st>>>(
+        g, i1_off, n1_loc, (const cufftDoubleComplex*)a, (const cufftComplex*)b, (cufftComplex*)b, r, invN,
+        a != nullptr, project);
+    FRG_CHECK_LAUNCH();
+}
+
+// per-block partial sums of sum_k w_k |m'|^2 |x_k|^2 over the split spectrum
+__global__ void k_slab_grad_energy(Dims g, int i1_off, int n1_loc, const cufftDoubleComplex* __restrict__ x,
+                                   double* __restrict__ partial) {
+    __shared__ double sw[8];
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    double acc = 0.0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+         e += (long long)gridDim.x * blockDim.x) {
+        int i0, i1, i2;
+        slab_spec_vox(g, i1_off, n1_loc, e, i0, i1, i2);
+        const Bin bn = bin_of(g, i0, i1, i2);
+        double kk = 0.0;
+        for (int q = 0; q < 3; ++q) kk += bn.nyq[q] ? 0.0 : bn.m[q] * bn.m[q];
+        const double w = (i2 == 0 || 2 * i2 == g.n2) ? 1.0 : 2.0;  // conjugate half of the spectrum
+        const cufftDoubleComplex v = x[e];
+        acc += w * kk * (v.x * v.x + v.y * v.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sw[q];
+        partial[blockIdx.x] = t;
+    }
+}
+
+double slab_grad_energy(const Dims& g, int i1_off, int n1_loc, const void* x_spec, cudaStream_t st) {
+    const long long cnt = (long long)g.n0 * n1_loc * (g.n2 / 2 + 1);
+    const int nb = slab_blocks(cnt);
+    double* part = nullptr;
+    FRG_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * nb, st));
+    k_slab_grad_energy<<<nb, 256, 0, st>>>(g, i1_off, n1_loc, (const cufftDoubleComplex*)x_spec, part);
+    FRG_CHECK_LAUNCH();
+    std::vector<double> h(nb);
+    FRG_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+    FRG_CUDA(cudaFreeAsync(part, st));
+    FRG_CUDA(cudaStreamSynchronize(st));
+    double t = 0.0;  // fixed order: deterministic
+    for (double v : h) t += v;
+    return t / ((double)g.n0 * g.n1 * g.n2);  // Parseval: sum_x |f|^2 = sum_k |F_k|^2 / N
 }
 
 void bspline_prefilter(const Dims& g, int dtype, const void* in, void* out, cudaStream_t st) {

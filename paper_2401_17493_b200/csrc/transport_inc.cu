@@ -240,14 +240,14 @@ void inc_first(const Dims& g, int method, int n_t, const float* disp, const floa
 }
 
 void inc_step(const Dims& g, int method, const float* disp, const float* m_src, const float* Sj, float* m_next,
-              cudaStream_t st) {
+              cudaStream_t st, float* fin, float fsign) {
     IncStepOp<float> op;
     op.ds = disp_src(g, disp);
     op.mj = m_src;
     op.Sj = Sj;
     op.mnext = m_next;
-    op.fin = nullptr;
-    op.fsign = 0.f;
+    op.fin = fin;
+    op.fsign = fsign;
     launch_sl<float, 1>(g, method, op, st);
 }
 

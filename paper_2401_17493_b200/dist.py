@@ -42,7 +42,7 @@ from .diffops import frg_reg
 from .kkt import PrecondKind, RegConfig
 
 __all__ = ["SlabComm", "SlabGrid", "SlabFFT", "DistKktState", "dist_register", "dist_continuation_solve",
-           "dist_search_alpha", "slab_bounds", "halo_width"]
+           "dist_search_alpha", "slab_bounds", "halo_width", "slab_synth"]
 
 TWO_PI = 2.0 * math.pi
 
@@ -210,6 +210,10 @@ class SlabFFT:
         P = self.comm.size
         y = torch.empty((C, n0l, n1, self.nh), dtype=cdt, device="cuda")
         L.check(L.lib().frg_slab_fft2(self.nloc, dt, C, 1, _c(x), _c(y), L.stream()), "slab_fft2")
+        if P == 1:  # the axis-1 split is the whole axis: no transpose, no exchange
+            L.check(L.lib().frg_slab_fft1(self.g.n_glob[0], self.n1l, self.g.n_glob[2], dt, C, 1, _c(y), L.stream()),
+                    "slab_fft1")
+            return y
         packed = torch.empty((C, P, n0l, self.n1l, self.nh), dtype=cdt, device="cuda")
         L.check(L.lib().frg_slab_transpose(1, P, self.nloc, dt, C, _c(y), _c(packed), L.stream()), "slab_transpose")
         spec = self.spectrum(C, x.dtype)
@@ -227,6 +231,9 @@ class SlabFFT:
         P = self.comm.size
         L.check(L.lib().frg_slab_fft1(self.g.n_glob[0], self.n1l, self.g.n_glob[2], dt, C, -1, _c(spec), L.stream()),
                 "slab_fft1")
+        if P == 1:
+            L.check(L.lib().frg_slab_fft2(self.nloc, dt, C, -1, _c(spec), _c(out), L.stream()), "slab_fft2")
+            return out
         packed = torch.empty((C, P, n0l, self.n1l, self.nh), dtype=spec.dtype, device="cuda")
         for c in range(C):
             self.comm.all_to_all(packed[c], spec[c].view(P, n0l, self.n1l, self.nh))
@@ -347,9 +354,16 @@ class DistKktState:
         except Exception:
             pass
 
+    def _absmax(self, a: torch.Tensor) -> float:
+        """Global max |a| (one fused reduction + one scalar all-reduce; the
+        host needs it to size the ghost planes, once per displacement map)."""
+        out = ctypes.c_double()
+        L.check(L.lib().frg_norm_inf(L.dtype_code(a.dtype), L.ptr(a), a.numel(), ctypes.byref(out), L.stream()),
+                "norm_inf")
+        return self.comm.all_reduce(out.value, "max")
+
     def _halo_of(self, disp: torch.Tensor) -> int:
-        local = float(disp[0].abs().max().item())
-        return max(halo_width(self.comm.all_reduce(local, "max"), self.method), 1)
+        return max(halo_width(self._absmax(disp[0]), self.method), 1)
 
     def dot(self, a: torch.Tensor, b: torch.Tensor) -> float:
         """Global sum(a * b) (unweighted), fused local kernel + all-reduce."""
@@ -377,17 +391,16 @@ class DistKktState:
     def _departure(self, v32: torch.Tensor, sign: float) -> torch.Tensor:
         vs = v32 if sign > 0 else -v32
         h0 = TWO_PI / self.grid.n_glob[0]
-        Wv = max(halo_width(self.comm.all_reduce(float(vs[0].abs().max().item()) * self.grid.h_t / h0, "max"),
-                            self.method), 4)
+        Wv = max(halo_width(self._absmax(v32[0]) * self.grid.h_t / h0, self.method), 4)
         v_ext = self._src(vs, Wv)
         disp = torch.empty_like(vs)
         L.check(L.lib().frg_slab_departure(self.n_loc, self.grid.n_glob[0], Wv, self._m, self.grid.h_t, _c(v_ext),
                                            _c(vs), _c(disp), L.stream()), "slab_departure")
         return disp, v_ext, Wv
 
-    def _state_solve(self, disp, W, keep: bool):
+    def _state_solve(self, disp, W, keep: bool, m0: torch.Tensor | None = None):
         g = self.grid
-        m = self.m0
+        m = self.m0 if m0 is None else m0
         series = [m] if keep else None
         for _ in range(g.n_t):
             nxt = torch.empty_like(m)
@@ -398,12 +411,18 @@ class DistKktState:
         return series if keep else m
 
     def _spectral_out(self, a64: torch.Tensor | None, b32: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-        """out (fp64) = alpha L a + P(b) in the spectral precision."""
-        sdt = self._spec_dt
-        a = a64.to(sdt) if a64 is not None else None
-        res = torch.empty(b32.shape, dtype=sdt, device="cuda")
-        self.fft.reg_plus_project(a, b32.to(sdt), self._reg, self._project, res)
-        out.copy_(res)
+        """out (fp64) = alpha L a + P(b), the single-GPU mixed arithmetic
+        (kkt.cu reg_plus_project_mixed): the f64 spectrum of a, the fp32
+        spectrum of b, an fp32 combine per bin, an fp32 inverse, one widening
+        pass into out — half the all-to-all bytes of f64 b spectra."""
+        sb = self.fft.forward(b32)
+        sa = self.fft.forward(a64) if a64 is not None else None
+        L.check(L.lib().frg_slab_spec_combine_mixed(self.fft.nglob, self.fft.i1_off, self.fft.n1l,
+                                                    None if sa is None else _c(sa), _c(sb), ctypes.byref(self._reg),
+                                                    int(self._project), L.stream()), "slab_spec_combine_mixed")
+        res = torch.empty(b32.shape, dtype=torch.float32, device="cuda")
+        self.fft.inverse(sb, res)
+        L.check(L.lib().frg_convert(L.F32, _c(res), L.F64, _c(out), res.numel(), L.stream()), "convert")
         return out
 
     def _body_force(self, lam):
@@ -425,6 +444,7 @@ class DistKktState:
         self.plan_f, self.plan_b = self._plan(self.disp_f), self._plan(self.disp_b)
         self._bind()
         divv = torch.empty(g.n, dtype=torch.float32, device="cuda")
+        self.divv = divv
         if self._bs:  # the departure solve exchanged coefficients; FD8 needs the nodal values
             v_ext = self._ext(v32, Wv)
         L.check(L.lib().frg_slab_fd8_divergence(self.n_loc, g.n_glob[0], Wv, _c(v_ext), _c(divv), L.stream()),
@@ -476,7 +496,10 @@ class DistKktState:
             vt_ext, vt_loc_p = self._src(vt_loc, Wf), _c(vt_loc)
         else:
             vt_ext = torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
-            vt_ext[:, Wf:Wf + n0l].copy_(vt)  # f64 -> f32 straight into the owned planes
+            vt64 = vt.to(torch.float64).contiguous()
+            for c in range(3):  # f64 -> f32 straight into the owned planes (vectorised convert)
+                L.check(L.lib().frg_convert(L.F64, _c(vt64[c]), L.F32, _c(vt_ext[c, Wf:Wf + n0l]), self.N,
+                                            L.stream()), "convert")
             self.comm.halo(vt_ext, Wf)
             vt_loc_p = None
         mt = torch.empty((g.n_t + 1, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
@@ -492,12 +515,16 @@ class DistKktState:
             self.comm.halo(series[j:j + 1], W)
             return series[j]
 
+        lt = torch.empty((g.n_t + 1, n0l + 2 * Wb, *g.n[1:]), dtype=torch.float32, device="cuda")
         for j in range(1, g.n_t):
             src = source(mt, j, Wf)
+            last = j == g.n_t - 1  # the last step writes lam~(1) = -m~(1) (SSD) straight into the adjoint series
             L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], Wf, self._m, _c(self.disp_f), _c(src),
-                                              _c(S[j - 1]), _c(own_f(j + 1)), L.stream()), "slab_inc_step")
-        lt = torch.empty((g.n_t + 1, n0l + 2 * Wb, *g.n[1:]), dtype=torch.float32, device="cuda")
-        torch.neg(own_f(g.n_t), out=lt[g.n_t, Wb:Wb + n0l])  # SSD: lam~(1) = -m~(1)
+                                              _c(S[j - 1]), None if last else _c(own_f(j + 1)),
+                                              _c(lt[g.n_t, Wb:Wb + n0l]) if last else None, -1.0, L.stream()),
+                    "slab_inc_step")
+        if g.n_t == 1:
+            torch.neg(own_f(1), out=lt[1, Wb:Wb + n0l])
         for j in range(g.n_t, 0, -1):
             src = source(lt, j, Wb)
             L.check(L.lib().frg_slab_adjoint_step(self.n_loc, g.n_glob[0], Wb, self._m, _c(self.disp_b),
@@ -517,10 +544,9 @@ class DistKktState:
         """kkt.py:308-311 ('reg': the spectral inverse of alpha L)."""
         if kind is not None and kind.kind != "reg":
             raise ValueError("the slab path implements the 'reg' preconditioner")
-        rd = r.data if hasattr(r, "data") else r
-        res = self.fft.apply(rd.to(self._spec_dt), "reg_inv", self._reg)
+        rd = (r.data if hasattr(r, "data") else r).to(self._spec_dt).contiguous()
         out = torch.empty_like(rd) if out is None else out
-        out.copy_(res)
+        self.fft.apply(rd, "reg_inv", self._reg, out=out)
         return _Vec(self.grid, out)
 
     def _reg_energy(self, v64: torch.Tensor) -> float:
@@ -550,7 +576,21 @@ class DistKktState:
         return self._dist / self._init_mismatch
 
     def divergence_energy(self) -> float:
-        return 0.0
+        """kkt.py:207-218: 0.5 beta (<div v, div v> + <grad div v, grad div v>)
+        (spectral gradient) in the near-incompressible mode, else 0 — the
+        gradient energy from this rank's share of the slab spectrum
+        (frg_slab_grad_energy), all-reduced."""
+        if self.reg.incomp.mode != "near-incompressible":
+            return 0.0
+        cv = self.grid.cell_volume
+        w = self.divv
+        ww = self.dot(w, w) * cv
+        spec = self.fft.forward(w.to(torch.float64).unsqueeze(0).contiguous())
+        out = ctypes.c_double()
+        L.check(L.lib().frg_slab_grad_energy(self.fft.nglob, self.fft.i1_off, self.fft.n1l, _c(spec),
+                                             ctypes.byref(out), L.stream()), "slab_grad_energy")
+        gg = self.comm.all_reduce(out.value) * cv
+        return 0.5 * self.reg.incomp.beta * (ww + gg)
 
     def detgrad_stats(self):
         """(min, mean, max) of det F(1) over the whole grid (kkt.py
@@ -673,3 +713,62 @@ def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, 
     total.trace = [row for rep in stages for row in rep.trace]
     return v, total, stages
 
+
+
+class _SlabTransport(DistKktState):
+    """The slab transport machinery of DistKktState (departure maps, tile
+    plans, ghost-plane gathers) without images or KKT state."""
+
+    def __init__(self, comm: SlabComm, n_glob, n_t: int, method: str = "cubic"):
+        self.comm = comm
+        self.grid = SlabGrid(tuple(int(v) for v in n_glob), comm.rank, comm.size, n_t=n_t)
+        self.method, self._m, self._bs = method, L.METHODS[method], method == "bspline"
+        self.reg = RegConfig()
+        self._reg = frg_reg(self.reg.operator, self.reg.alpha, self.reg.incomp)
+        self.fft = SlabFFT(self.grid, comm)
+        self.n_loc = L.n3(self.grid.n)
+        self.N = int(np.prod(self.grid.n))
+
+
+def slab_synth(name: str, n: int, comm: SlabComm, seed: int = 1, amp: float = 0.7, ref_steps: int = 64):
+    """synth.synth_case for configs C4 / C5 generated slab by slab: this rank's
+    planes of the bump template (synth.py:28-43, global min / max
+    normalisation all-reduced) and of the rotation velocity (synth.py:46-63),
+    and the reference image from a ``ref_steps``-step cubic SL transport run
+    by the slab path itself (synth.py:113-117) — no rank ever holds the whole
+    grid, so 1024^3 over 8 GPUs fits.  Transport in fp32 (the slab path's
+    precision; the single-GPU generator is f64).  Returns (m0, m1) fp32 and v
+    f64, each (.., n/P, n, n)."""
+    if name != "rotation":
+        raise ValueError("slab_synth implements the rotation case")
+    lo, hi = slab_bounds(n, comm.size, comm.rank)
+    rng = np.random.default_rng(seed)
+    hh = TWO_PI / n
+    ax = ((n // 2) - (torch.arange(n, dtype=torch.float64, device="cuda") + 1.0)) * hh
+    x0 = ax[lo:hi].view(-1, 1, 1)
+    x1 = ax.view(1, -1, 1)
+    x2 = ax.view(1, 1, -1)
+    vals = torch.zeros((hi - lo, n, n), dtype=torch.float64, device="cuda")
+    for _ in range(6):
+        c = rng.uniform(-np.pi, np.pi, size=3)
+        kappa = rng.uniform(1.0, 2.5)
+        a = rng.uniform(0.4, 1.0)
+        vals += a * (torch.exp(kappa * (torch.cos(x0 - c[0]) - 1.0)) * torch.exp(kappa * (torch.cos(x1 - c[1]) - 1.0))
+                     * torch.exp(kappa * (torch.cos(x2 - c[2]) - 1.0)))
+    vmin = -comm.all_reduce(-float(vals.min()), "max")
+    vals -= vmin
+    vmax = comm.all_reduce(float(vals.max()), "max")
+    if vmax > 0:
+        vals /= vmax
+    mod = 1.0 + 0.3 * torch.cos(x2)
+    v = torch.zeros((3, hi - lo, n, n), dtype=torch.float64, device="cuda")
+    v[0] = -amp * torch.cos(x0) * torch.sin(x1) * mod
+    v[1] = amp * torch.sin(x0) * torch.cos(x1) * mod
+    m0 = vals.float().contiguous()
+    tr = _SlabTransport(comm, (n, n, n), ref_steps, "cubic")
+    disp, _, _ = tr._departure(v.float(), 1.0)
+    plan = tr._plan(disp)
+    L.check(L.lib().frg_bind_plan(0, _c(disp), _c(plan), tr._m), "bind_plan")
+    m1 = tr._state_solve(disp, tr._halo_of(disp), keep=False, m0=m0)
+    L.check(L.lib().frg_clear_plans(), "clear_plans")
+    return m0, m1.contiguous(), v

@@ -71,6 +71,16 @@ def _worker(rank, size, port, n, outdir, do_register, method):
     res["objective_at"] = abs(st.objective_at(1.1 * v[:, lo:hi].contiguous())
                               - ref.objective_at(F.VectorField._wrap(m0.grid, 1.1 * v))) / abs(ref.objective())
     res["mismatch"] = abs(st.mismatch() - ref.mismatch())
+    # a velocity with divergence (the rotation field is divergence free)
+    x2 = torch.arange(n, dtype=torch.float64, device="cuda") * (2 * np.pi / n)
+    vd = v.clone()
+    vd[2] += 0.2 * torch.sin(2 * x2).view(1, 1, n)
+    st_d = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
+                          v_init=vd[:, lo:hi].contiguous(), method=method)
+    ref_d = F.KktState(m0, m1, reg, v_init=F.VectorField._wrap(m0.grid, vd), transport_dtype=np.float32,
+                       method=method)
+    res["divergence_energy"] = [st_d.divergence_energy(), ref_d.divergence_energy()]
+    del st_d, ref_d
     if do_register is True:
         cfg = OptimizerConfig()
         _, rep_d = D.dist_register(m0.values[lo:hi].float(), m1.values[lo:hi].float(), comm, (n, n, n), config=cfg,
@@ -125,6 +135,8 @@ def test_slab_kkt_matches_single_gpu(size, tmp_path):
             assert res[key] < 1e-5, (size, rank, key, res[key])
         assert res["objective"] < 1e-6 and res["objective_at"] < 1e-6, res
         assert res["mismatch"] < 1e-6, res
+        de, de1 = res["divergence_energy"]  # kkt.py:207-218 (near-incompressible)
+        assert de1 > 0 and abs(de - de1) < 1e-6 * de1, res
 
 
 @pytest.mark.parametrize("method", ["bspline", "linear"])
@@ -167,3 +179,36 @@ def test_slab_search_alpha_matches_single_gpu(tmp_path):
         assert s["best"][0] == s["best"][1] and s["status"][0] == s["status"][1], s
         for a, b in zip(s["det_dist"], s["det_single"]):
             assert np.allclose(a, b, rtol=1e-4, atol=1e-6), (a, b)
+
+
+def _synth_worker(rank, size, port, n, outdir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=size)
+    import paper_2401_17493_b200 as F
+    from paper_2401_17493_b200 import dist as D
+
+    m0, m1, v = D.slab_synth("rotation", n, D.SlabComm())
+    r0, r1, rv = F.synth_case("rotation", n, seed=1, d=3)
+    lo, hi = D.slab_bounds(n, size, rank)
+    res = {"m0": _rel(m0, r0.values[lo:hi]), "m1": _rel(m1, r1.values[lo:hi]), "v": _rel(v, rv.data[:, lo:hi])}
+    with open(os.path.join(outdir, f"synth{rank}.json"), "w") as fh:
+        json.dump(res, fh)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_slab_synth_matches_single_gpu_generator(tmp_path):
+    """dist.slab_synth (configs C4 / C5 inputs, generated slab by slab) vs the
+    single-GPU synth_case: template and velocity to rounding, the reference
+    image (64-step transport, fp32 slab path vs f64) within 1e-5."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_synth_worker, args=(2, _free_port(), 64, str(tmp_path)), nprocs=2, start_method="spawn",
+                       join=True)
+    for r in range(2):
+        res = json.load(open(os.path.join(tmp_path, f"synth{r}.json")))
+        assert res["m0"] < 1e-7 and res["v"] < 1e-15 and res["m1"] < 1e-5, res

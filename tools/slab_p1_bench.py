@@ -42,4 +42,10 @@ del st
 ds = D.DistKktState(m0.values.float(), m1.values.float(), reg, D.SlabComm(), (n, n, n), v_init=v)
 r2 = rate(lambda: ds.hessian_matvec(vt, out=out))
 print(f"n={n}: single-GPU context {r1:.1f} matvec/s, slab path P=1 {r2:.1f} matvec/s")
+if os.environ.get("PROFILE"):  # one slab matvec between cudaProfilerStart/Stop (ncu --profile-from-start off)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    ds.hessian_matvec(vt, out=out)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 tdist.destroy_process_group()
