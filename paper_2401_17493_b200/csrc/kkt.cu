@@ -9,6 +9,7 @@
 // control_dtype, so H2/H3 keeps fp64 control vectors (SURVEY.md §7 hard part 1)
 // while the transport runs in fp32.
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <vector>
 
@@ -154,6 +155,14 @@ struct KktCtx {
     double initial_mismatch = 0.0, dist_cur = 0.0;
     bool dist_valid = false;
     long long matvecs = 0, pde_solves = 0, precond_fallbacks = 0;
+    // CUDA graph of the GN matvec (small grids: the launch sequence, not the
+    // kernels, bounds a 64^3 matvec); captured with context-owned in / out
+    // buffers, keyed by every device pointer the sequence touches
+    cudaGraphExec_t mv_exec = nullptr;
+    std::vector<const void*> mv_key;
+    DevBuf g_in, g_out;
+    long long mv_calls = 0;
+    cudaStream_t cap_st = nullptr;
 
     size_t T() const { return es(tdt); }
     size_t C() const { return es(cdt); }
@@ -224,6 +233,10 @@ void kkt_destroy(KktCtx* k) {
                       &k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q, &k->c_u, &k->plan_f, &k->plan_b,
                       &k->plan_t};
     for (DevBuf* b : bufs) b->free_();
+    k->g_in.free_();
+    k->g_out.free_();
+    if (k->mv_exec) cudaGraphExecDestroy(k->mv_exec);
+    if (k->cap_st) cudaStreamDestroy(k->cap_st);
     k->ws_a.release();
     k->ws_b.release();
     k->ws_c.release();
@@ -506,8 +519,63 @@ void kkt_gradient(KktCtx* k, void* g_out) {
     reg_plus_body(k, k->v.p, k->vT.p, k->lam.p, g_out);
 }
 
+static void matvec_body(KktCtx* k, const void* vt, void* out);
+
+// graphs: whole-grid contexts up to FRG_GRAPH_MAX_N voxels (default 128^3;
+// 0 disables), SSD, fp32/f64 cubic or linear taps (the fp16 and B-spline
+// paths use thread-local scratch whose address may move between calls)
+static bool graph_ok(const KktCtx* k) {
+    static const long long maxn = getenv("FRG_GRAPH_MAX_N") ? atoll(getenv("FRG_GRAPH_MAX_N")) : (1LL << 21);
+    return k->g.N <= maxn && k->distance == 0 && k->interp_bits == 32 && k->method != BSPLINE && k->g.h0 == 0;
+}
+
+static std::vector<const void*> graph_key(KktCtx* k) {
+    return {k->disp_f.p, k->disp_b.p, k->plan_f.p, k->plan_b.p, k->grads.p, k->grads_y.p, k->vtT.p, k->vty.p,
+            k->mt.p, k->lt.p, k->cmul.p, k->bf.p, k->ws_a.ptr, k->ws_b.ptr, k->g_in.p, k->g_out.p,
+            (const void*)(intptr_t)k->tdt, (const void*)(intptr_t)k->cdt};
+}
+
 void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
     FRG_REQUIRE(k->have_state, "refresh first");
+    const size_t bytes = (size_t)k->g.d * k->N() * k->C();
+    if (graph_ok(k) && ++k->mv_calls >= 2) {  // the first call allocates every workspace the sequence uses
+        k->g_in.alloc(bytes);
+        k->g_out.alloc(bytes);
+        std::vector<const void*> key = graph_key(k);
+        if (!k->mv_exec || key != k->mv_key) {
+            if (k->mv_exec) FRG_CUDA(cudaGraphExecDestroy(k->mv_exec));
+            k->mv_exec = nullptr;
+            if (!k->cap_st) FRG_CUDA(cudaStreamCreateWithFlags(&k->cap_st, cudaStreamNonBlocking));
+            FRG_CUDA(cudaStreamSynchronize(k->st));
+            cudaStream_t user = k->st;
+            k->st = k->cap_st;  // capture on a private stream (the caller's may be the legacy one)
+            cudaGraph_t graph = nullptr;
+            FRG_CUDA(cudaStreamBeginCapture(k->cap_st, cudaStreamCaptureModeThreadLocal));
+            try {
+                matvec_body(k, k->g_in.p, k->g_out.p);
+            } catch (...) {
+                cudaStreamEndCapture(k->cap_st, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                k->st = user;
+                throw;
+            }
+            k->st = user;
+            FRG_CUDA(cudaStreamEndCapture(k->cap_st, &graph));
+            FRG_CUDA(cudaGraphInstantiate(&k->mv_exec, graph, 0));
+            FRG_CUDA(cudaGraphDestroy(graph));
+            k->mv_key = graph_key(k);
+        }
+        FRG_CUDA(cudaMemcpyAsync(k->g_in.p, vt, bytes, cudaMemcpyDeviceToDevice, k->st));
+        FRG_CUDA(cudaGraphLaunch(k->mv_exec, k->st));
+        FRG_CUDA(cudaMemcpyAsync(out, k->g_out.p, bytes, cudaMemcpyDeviceToDevice, k->st));
+    } else {
+        matvec_body(k, vt, out);
+    }
+    k->matvecs += 1;
+    k->pde_solves += 2;
+}
+
+static void matvec_body(KktCtx* k, const void* vt, void* out) {
     const long long N = k->N();
     const size_t T = k->T();
     void* lt_final = k->lt.at<char>((size_t)k->n_t * N * T);
@@ -526,8 +594,6 @@ void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
         incremental_final_ncc(k, k->tmp1.p, m_final(k), lt_final);
     }
     solve_adjoint(k->g, k->tdt, k->method, k->n_t, k->disp_b.p, k->cmul.p, k->lt.p, k->st);
-    k->matvecs += 1;
-    k->pde_solves += 2;
     reg_plus_body(k, vt, k->vtT.p, k->lt.p, out);
 }
 

@@ -417,3 +417,26 @@ def test_release_device_pool():
     F.release_device_pool()
     free1 = torch.cuda.mem_get_info()[0]
     assert free1 > free0
+
+
+@pytest.mark.parametrize("tdt", [np.float32, None])
+def test_graph_matvec_matches_eager(tdt):
+    """Small grids replay the GN matvec as a CUDA graph from the second call
+    on (csrc/kkt.cu kkt_hessian_matvec): bit-identical to the eager first call,
+    still correct after a refresh, counters unchanged."""
+    m0, m1, vtrue = F.synth_case("rotation", 64, seed=1, d=3)
+    grid = m0.grid
+    W = lambda x: VectorField._wrap(grid, x)  # noqa: E731
+    st = KktState(m0, m1, _reg({"incomp": "near-incompressible"}), v_init=W(0.5 * vtrue.data), transport_dtype=tdt)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = W(0.1 * torch.randn((3, 64, 64, 64), generator=gen, dtype=torch.float64, device="cuda"))
+    h1 = st.hessian_matvec(x).data.clone()
+    h2 = st.hessian_matvec(x).data.clone()
+    h3 = st.hessian_matvec(x).data.clone()
+    assert torch.equal(h1, h2) and torch.equal(h2, h3)
+    st.refresh(W(0.4 * vtrue.data))
+    h4 = st.hessian_matvec(x).data.clone()
+    fresh = KktState(m0, m1, _reg({"incomp": "near-incompressible"}), v_init=W(0.4 * vtrue.data),
+                     transport_dtype=tdt)
+    assert torch.equal(h4, fresh.hessian_matvec(x).data)
+    assert st.matvecs == 4 and st.pde_solves == 2 * 2 + 4 * 2
