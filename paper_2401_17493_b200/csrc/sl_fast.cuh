@@ -63,7 +63,7 @@ struct alignas(64) TmaMaps {
 
 // host: 2D tiled tensor map over an fp32 (n0, n1, n2) field viewed as
 // (n0*n1, n2), box TB_J rows x TB_K columns
-void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g);
+void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g, int box_k = TB_K, int box_j = TB_J);
 // host: whether the TMA engine applies to this grid (every axis >= its box edge)
 inline bool tma_grid_ok(const Dims& g) {
     return (g.h0 > 0 || g.n0 >= TB_I) && g.n1 >= TB_J && g.n2 >= TB_K && (g.n2 % 4) == 0;
@@ -97,10 +97,11 @@ __device__ __forceinline__ void tma_load_2d(float* dst, const CUtensorMap* map, 
         : "memory");
 }
 // issue the S0 plane loads of one field box (one thread)
+template <int PLANE = TB_PLANE>
 __device__ __forceinline__ void tma_box(float* box, const CUtensorMap* map, const Dims& g, int lo0, int lo1, int lo2,
                                         int S0, uint64_t* bar) {
-    mbar_expect_tx(bar, (unsigned)(S0 * TB_PLANE * sizeof(float)));
-    for (int a = 0; a < S0; ++a) tma_load_2d(box + a * TB_PLANE, map, lo2, src_plane(g, lo0 + a) * g.n1 + lo1, bar);
+    mbar_expect_tx(bar, (unsigned)(S0 * PLANE * sizeof(float)));
+    for (int a = 0; a < S0; ++a) tma_load_2d(box + a * PLANE, map, lo2, src_plane(g, lo0 + a) * g.n1 + lo1, bar);
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
@@ -116,6 +117,7 @@ __device__ __forceinline__ void lagrange4f(float t, float (&w)[4]) {
 }
 
 // 64-tap cubic from a fixed-geometry box: every tap an immediate offset from p
+template <int K = TB_K, int PLANE = TB_PLANE>
 __device__ __forceinline__ float cubic_fixed(const float* __restrict__ p, const float (&w0)[4], const float (&w1)[4],
                                              const float (&w2)[4]) {
     float acc = 0.f;
@@ -124,7 +126,7 @@ __device__ __forceinline__ float cubic_fixed(const float* __restrict__ p, const 
         float plane = 0.f;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const float* row = p + a * TB_PLANE + b * TB_K;
+            const float* row = p + a * PLANE + b * K;
             float r = w2[0] * row[0];
             r = fmaf(w2[1], row[1], r);
             r = fmaf(w2[2], row[2], r);
@@ -136,19 +138,22 @@ __device__ __forceinline__ float cubic_fixed(const float* __restrict__ p, const 
     return acc;
 }
 
+template <int K = TB_K, int PLANE = TB_PLANE>
 __device__ __forceinline__ float linear_fixed(const float* __restrict__ b, float t0, float t1, float t2) {
     // same expression order as box_interp<LINEAR> / apply_stencil<LINEAR>
     float c00 = (1.f - t2) * b[0] + t2 * b[1];
-    float c01 = (1.f - t2) * b[TB_K] + t2 * b[TB_K + 1];
-    float c10 = (1.f - t2) * b[TB_PLANE] + t2 * b[TB_PLANE + 1];
-    float c11 = (1.f - t2) * b[TB_PLANE + TB_K] + t2 * b[TB_PLANE + TB_K + 1];
+    float c01 = (1.f - t2) * b[K] + t2 * b[K + 1];
+    float c10 = (1.f - t2) * b[PLANE] + t2 * b[PLANE + 1];
+    float c11 = (1.f - t2) * b[PLANE + K] + t2 * b[PLANE + K + 1];
     return (1.f - t0) * ((1.f - t1) * c00 + t1 * c01) + t0 * ((1.f - t1) * c10 + t1 * c11);
 }
 
 // copy the box elements whose coordinate along `axis` leaves [0, n) from their
 // periodic images (after the TMA zero-filled them); 4-byte cp.async
+template <int J = TB_J, int K = TB_K>
 __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
-                                           int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid) {
+                                           int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid,
+                                           int nthreads = BX * BY) {
     const int lo = axis == 0 ? lo0 : (axis == 1 ? lo1 : lo2);
     const int S = axis == 0 ? S0 : (axis == 1 ? S1 : S2);
     const int n = g.axis_len(axis);
@@ -161,7 +166,7 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
     const int E1 = axis == 0 ? S1 : S0;           // outer of the remaining pair
     const int E2 = axis == 2 ? S1 : S2;           // inner of the remaining pair
     const int total = cnt * E1 * E2;
-    for (int e = tid; e < total; e += BX * BY) {
+    for (int e = tid; e < total; e += nthreads) {
         int r = e / E2;
         const int in2 = e - r * E2;
         const int q = r / E1;
@@ -176,7 +181,7 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
             a = in1; b = in2; c = x;
         }
         const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
-        cp_async_elem<4>(box + (a * TB_J + b) * TB_K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
+        cp_async_elem<4>(box + (a * J + b) * K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
     }
 }
 
@@ -329,6 +334,7 @@ __device__ __forceinline__ void weights4f_x2(float2 t, float2 (&w)[4]) {
 // two cubic stencils with paired FMAs: the taps of point A and point B load
 // into the two halves of one register pair; lane-for-lane identical to
 // cubic_fixed
+template <int K = TB_K, int PLANE = TB_PLANE>
 __device__ __forceinline__ float2 cubic_fixed_x2(const float* __restrict__ pA, const float* __restrict__ pB,
                                                  const float2 (&w0)[4], const float2 (&w1)[4],
                                                  const float2 (&w2)[4]) {
@@ -338,8 +344,8 @@ __device__ __forceinline__ float2 cubic_fixed_x2(const float* __restrict__ pA, c
         float2 plane = make_float2(0.f, 0.f);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const float* rA = pA + a * TB_PLANE + b * TB_K;
-            const float* rB = pB + a * TB_PLANE + b * TB_K;
+            const float* rA = pA + a * PLANE + b * K;
+            const float* rB = pB + a * PLANE + b * K;
             float2 r = __fmul2_rn(w2[0], make_float2(rA[0], rB[0]));
             r = __ffma2_rn(w2[1], make_float2(rA[1], rB[1]), r);
             r = __ffma2_rn(w2[2], make_float2(rA[2], rB[2]), r);

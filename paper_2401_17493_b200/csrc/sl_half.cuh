@@ -16,6 +16,7 @@
 #include <cuda_fp16.h>
 
 #include "sl_fast.cuh"
+#include "sl_pipe.cuh"
 
 namespace frg {
 
@@ -304,6 +305,9 @@ void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
                 if (method == LINEAR && launch_slh<LINEAR, Op>(g, op, st)) return;
             }
         }
+        if (method == CUBIC && launch_slp<CUBIC, NF, Op>(g, op, st)) return;
+        if (method == BSPLINE && launch_slp<BSPLINE, NF, Op>(g, op, st)) return;
+        if (method == LINEAR && launch_slp<LINEAR, NF, Op>(g, op, st)) return;
         if (method == CUBIC) return launch_slf<CUBIC, NF, Op>(g, op, st);
         if (method == BSPLINE) return launch_slf<BSPLINE, NF, Op>(g, op, st);
         if (method == LINEAR) return launch_slf<LINEAR, NF, Op>(g, op, st);

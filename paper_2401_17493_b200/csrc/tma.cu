@@ -23,11 +23,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g) {
+void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g, int box_k, int box_j) {
     FRG_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA field must be 16-byte aligned");
     const cuuint64_t dims[2] = {(cuuint64_t)g.n2, (cuuint64_t)(g.n0 + 2 * g.h0) * g.n1};
     const cuuint64_t strides[1] = {(cuuint64_t)g.n2 * 4};
-    const cuuint32_t box[2] = {TB_K, TB_J};
+    const cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_j};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
