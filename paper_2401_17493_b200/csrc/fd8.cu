@@ -72,9 +72,14 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_div(Dims g, const T* __restrict
 // of 25 (mostly L2 re-reads of neighbouring planes).  Same per-term order as
 // fd8_line, so results are identical.
 #ifndef FRG_FD8_CHUNK
-#define FRG_FD8_CHUNK 32
+#define FRG_FD8_CHUNK 16
 #endif
 constexpr int FD8_CHUNK = FRG_FD8_CHUNK;
+// measured at 256^3 (5 fp32 slices / one divergence): chunk 32 -> 16 and 6
+// CTAs per SM for the gradient: 448-499 -> 409 us; divergence 116 -> 111 us
+#ifndef FRG_FD8_MINB
+#define FRG_FD8_MINB 6
+#endif
 
 template <typename T>
 __device__ __forceinline__ T fd8_taps(const T (&up)[5], const T (&um)[5], T inv840h) {
@@ -89,25 +94,24 @@ __device__ __forceinline__ T fd8_taps(const T (&up)[5], const T (&um)[5], T inv8
     return acc * inv840h;
 }
 
+// periodic plane index for i in [-n0, 2 n0) (the column marches never leave it)
+__device__ __forceinline__ int wrap_plane(int i, int n0) { return i < 0 ? i + n0 : (i >= n0 ? i - n0 : i); }
+
 template <typename T>
-__global__ void __launch_bounds__(BX * BY) k_fd8_grad_col(Dims g, int nslices, int nchunk, const T* __restrict__ u,
+__global__ void __launch_bounds__(BX * BY, FRG_FD8_MINB) k_fd8_grad_col(Dims g, int nslices, int nchunk, const T* __restrict__ u,
                                                          T* __restrict__ out) {
     __shared__ T tile[BY + 8][BX + 8];
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
     const int k = blockIdx.x * BX + tx, j = blockIdx.y * BY + ty;
     const int slice = blockIdx.z / nchunk, ch = blockIdx.z - slice * nchunk;
     const int ib = ch * FD8_CHUNK, ie = min(ib + FD8_CHUNK, g.n0);
+    const int plane = g.n1 * g.n2;
     const T* __restrict__ us = u + (size_t)slice * g.N;
-    T* __restrict__ os = out + (size_t)slice * 3 * g.N;
     const bool in = k < g.n2 && j < g.n1;
-    const long long plane = (long long)g.n1 * g.n2;
+    const int cofs = in ? j * g.n2 + k : 0;  // this thread's column within a plane
     const T inv0 = T(1) / (T(840) * T(TWO_PI / g.n0)), inv1 = T(1) / (T(840) * T(TWO_PI / g.n1)),
             inv2 = T(1) / (T(840) * T(TWO_PI / g.n2));
-    auto col = [&](int i) -> T {
-        int ii = i % g.n0;
-        if (ii < 0) ii += g.n0;
-        return in ? __ldg(us + ii * plane + (long long)j * g.n2 + k) : T(0);
-    };
+    auto col = [&](int i) -> T { return __ldg(us + wrap_plane(i, g.n0) * plane + cofs); };
     T win[9];  // win[q] = u(i - 4 + q) of this column
 #pragma unroll
     for (int q = 0; q < 8; ++q) win[q] = col(ib - 4 + q);
@@ -115,33 +119,34 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_grad_col(Dims g, int nslices, i
     // tile element e = tid + 256 q (q < 3) of the plane being prefetched
     constexpr int TW = BX + 8, TE = (BY + 8) * (BX + 8);
     int toff[3];
-    bool tin[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const int e = tid + q * BX * BY;
-        tin[q] = e < TE;
         const int r = e / TW, c = e - r * TW;
         int jj = jb + r, kk = kb + c;
         jj = jj < 0 ? jj + g.n1 : (jj >= g.n1 ? jj - g.n1 : jj);
         kk = kk < 0 ? kk + g.n2 : (kk >= g.n2 ? kk - g.n2 : kk);
-        toff[q] = tin[q] ? jj * g.n2 + kk : 0;
+        toff[q] = e < TE ? jj * g.n2 + kk : 0;
     }
     T nxt[3];
     T wnext = col(ib + 4);
+    const T* pl = us + ib * plane;  // plane ib
 #pragma unroll
-    for (int q = 0; q < 3; ++q) nxt[q] = tin[q] ? __ldg(us + ib * plane + toff[q]) : T(0);
+    for (int q = 0; q < 3; ++q) nxt[q] = __ldg(pl + toff[q]);
     T* flat = &tile[0][0];
-    for (int i = ib; i < ie; ++i) {
+    T* __restrict__ o = out + (size_t)slice * 3 * g.N + ib * plane + cofs;
+    for (int i = ib; i < ie; ++i, o += plane) {
         __syncthreads();  // previous plane's tile fully consumed
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-            if (tin[q]) flat[tid + q * BX * BY] = nxt[q];
+            if (q < 2 || tid + q * BX * BY < TE) flat[tid + q * BX * BY] = nxt[q];
         win[8] = wnext;
         __syncthreads();
         if (i + 1 < ie) {  // next plane in flight while this one is differentiated
             wnext = col(i + 5);
+            pl += plane;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) nxt[q] = tin[q] ? __ldg(us + (i + 1) * plane + toff[q]) : T(0);
+            for (int q = 0; q < 3; ++q) nxt[q] = __ldg(pl + toff[q]);
         }
         if (in) {
             T up[5], um[5];
@@ -150,20 +155,120 @@ __global__ void __launch_bounds__(BX * BY) k_fd8_grad_col(Dims g, int nslices, i
                 up[sh] = win[4 + sh];
                 um[sh] = win[4 - sh];
             }
-            const size_t p = (size_t)i * plane + (size_t)j * g.n2 + k;
-            os[p] = fd8_taps<T>(up, um, inv0);
+            o[0] = fd8_taps<T>(up, um, inv0);
 #pragma unroll
             for (int sh = 1; sh <= 4; ++sh) {
                 up[sh] = tile[ty + 4 + sh][tx + 4];
                 um[sh] = tile[ty + 4 - sh][tx + 4];
             }
-            os[g.N + p] = fd8_taps<T>(up, um, inv1);
+            o[g.N] = fd8_taps<T>(up, um, inv1);
 #pragma unroll
             for (int sh = 1; sh <= 4; ++sh) {
                 up[sh] = tile[ty + 4][tx + 4 + sh];
                 um[sh] = tile[ty + 4][tx + 4 - sh];
             }
-            os[2 * g.N + p] = fd8_taps<T>(up, um, inv2);
+            o[2 * g.N] = fd8_taps<T>(up, um, inv2);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) win[q] = win[q + 1];
+    }
+}
+
+// 2.5D-blocked divergence (3D, single GPU): the axis-0 term from a register
+// window of v_0's column, the axis-1 / axis-2 terms from shared tiles of v_1
+// (row halo) and v_2 (column halo) of the current plane; 16 bytes of HBM per
+// voxel instead of ~25 L1/L2 loads.  Same summation order as k_fd8_div
+// ((0 + d0) + d1) + d2 and the same taps as fd8_line, so results are identical.
+template <typename T>
+__global__ void __launch_bounds__(BX * BY) k_fd8_div_col(Dims g, int nchunk, const T* __restrict__ vf,
+                                                        T* __restrict__ out) {
+    __shared__ T t1[BY + 8][BX];      // v_1, rows j - 4 .. j + BY + 3
+    __shared__ T t2[BY][BX + 8 + 1];  // v_2, columns k - 4 .. k + BX + 3 (+1: bank skew)
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+    const int k = blockIdx.x * BX + tx, j = blockIdx.y * BY + ty;
+    const int ib = blockIdx.z * FD8_CHUNK, ie = min(ib + FD8_CHUNK, g.n0);
+    const int plane = g.n1 * g.n2;
+    const T* __restrict__ v0 = vf;
+    const T* __restrict__ v1 = vf + (size_t)g.N;
+    const T* __restrict__ v2 = vf + 2 * (size_t)g.N;
+    const bool in = k < g.n2 && j < g.n1;
+    const int cofs = in ? j * g.n2 + k : 0;
+    const T inv0 = T(1) / (T(840) * T(TWO_PI / g.n0)), inv1 = T(1) / (T(840) * T(TWO_PI / g.n1)),
+            inv2 = T(1) / (T(840) * T(TWO_PI / g.n2));
+    const int kb = blockIdx.x * BX - 4, jb = blockIdx.y * BY - 4;
+    // t1: (BY + 8) x BX = 512 elements -> 2 per thread; t2: BY x (BX + 8) = 320 -> 2 per thread (second partial)
+    constexpr int E1 = (BY + 8) * BX, E2 = BY * (BX + 8);
+    int o1[2], o2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        int e = tid + q * BX * BY;
+        int r = e / BX, c = e - r * BX;
+        int jj = jb + r, kk = blockIdx.x * BX + c;
+        jj = jj < 0 ? jj + g.n1 : (jj >= g.n1 ? jj - g.n1 : jj);
+        kk = kk >= g.n2 ? kk - g.n2 : kk;
+        o1[q] = e < E1 ? jj * g.n2 + kk : 0;
+        r = e / (BX + 8);
+        c = e - r * (BX + 8);
+        jj = blockIdx.y * BY + r;
+        kk = kb + c;
+        jj = jj >= g.n1 ? jj - g.n1 : jj;
+        kk = kk < 0 ? kk + g.n2 : (kk >= g.n2 ? kk - g.n2 : kk);
+        o2[q] = e < E2 ? jj * g.n2 + kk : 0;
+    }
+    auto col = [&](int i) -> T { return __ldg(v0 + wrap_plane(i, g.n0) * plane + cofs); };
+    T win[9];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) win[q] = col(ib - 4 + q);
+    T wnext = col(ib + 4);
+    int pofs = ib * plane;
+    T n1v[2], n2v[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        n1v[q] = __ldg(v1 + pofs + o1[q]);
+        n2v[q] = __ldg(v2 + pofs + o2[q]);
+    }
+    T* __restrict__ o = out + pofs + cofs;
+    for (int i = ib; i < ie; ++i, o += plane) {
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = tid + q * BX * BY;
+            if (e < E1) (&t1[0][0])[e] = n1v[q];
+            if (e < E2) t2[e / (BX + 8)][e % (BX + 8)] = n2v[q];
+        }
+        win[8] = wnext;
+        __syncthreads();
+        if (i + 1 < ie) {
+            wnext = col(i + 5);
+            pofs += plane;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                n1v[q] = __ldg(v1 + pofs + o1[q]);
+                n2v[q] = __ldg(v2 + pofs + o2[q]);
+            }
+        }
+        if (in) {
+            T up[5], um[5];
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = win[4 + sh];
+                um[sh] = win[4 - sh];
+            }
+            T acc = T(0);
+            acc += fd8_taps<T>(up, um, inv0);
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = t1[ty + 4 + sh][tx];
+                um[sh] = t1[ty + 4 - sh][tx];
+            }
+            acc += fd8_taps<T>(up, um, inv1);
+#pragma unroll
+            for (int sh = 1; sh <= 4; ++sh) {
+                up[sh] = t2[ty][tx + 4 + sh];
+                um[sh] = t2[ty][tx + 4 - sh];
+            }
+            acc += fd8_taps<T>(up, um, inv2);
+            *o = acc;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) win[q] = win[q + 1];
@@ -195,6 +300,16 @@ void fd8_divergence(const Dims& g, int tdtype, const void* v, void* out, cudaStr
     FRG_REQUIRE(g.h0 == 0 || g.h0 >= 4, "slab FD8 needs >= 4 ghost planes");
     for (int c = 0; c < g.d; ++c)
         FRG_REQUIRE(g.axis_glob(g.comp_axis(c)) >= 9, "8th-order stencil needs n_i >= 9");
+    if (g.d == 3 && g.h0 == 0 && g.n0 >= 9 && g.n1 >= 9 && g.n2 >= 9) {
+        const int nchunk = (g.n0 + FD8_CHUNK - 1) / FD8_CHUNK;
+        dim3 grid((g.n2 + BX - 1) / BX, (g.n1 + BY - 1) / BY, nchunk);
+        if (tdtype == F64)
+            k_fd8_div_col<double><<<grid, vox_block(), 0, st>>>(g, nchunk, (const double*)v, (double*)out);
+        else
+            k_fd8_div_col<float><<<grid, vox_block(), 0, st>>>(g, nchunk, (const float*)v, (float*)out);
+        FRG_CHECK_LAUNCH();
+        return;
+    }
     if (tdtype == F64)
         k_fd8_div<double><<<vox_grid(g), vox_block(), 0, st>>>(g, (const double*)v, (double*)out);
     else

@@ -31,3 +31,22 @@ b.record()
 torch.cuda.synchronize()
 print(os.environ.get("FRG_LIB", "default"), "fd8 5 slices: %.1f us" % (a.elapsed_time(b) / 20 * 1e3),
       "checksum %.6e" % float(out.double().abs().sum()))
+
+v = torch.randn((3, n, n, n), generator=torch.Generator(device="cuda").manual_seed(1), dtype=torch.float32, device="cuda")
+dv = torch.empty((n, n, n), dtype=torch.float32, device="cuda")
+
+
+def rund():
+    L.check(L.lib().frg_fd8_divergence(nn, 3, L.F32, L.ptr(v), L.ptr(dv), L.stream()), "fd8 div")
+
+
+for _ in range(3):
+    rund()
+torch.cuda.synchronize()
+a.record()
+for _ in range(20):
+    rund()
+b.record()
+torch.cuda.synchronize()
+print(os.environ.get("FRG_LIB", "default"), "fd8 divergence: %.1f us" % (a.elapsed_time(b) / 20 * 1e3),
+      "checksum %.6e" % float(dv.double().abs().sum()))
