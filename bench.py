@@ -559,8 +559,61 @@ def run_slab(a, F, L, world, rank, local, backend):
     return None
 
 
+def host_info():
+    """lscpu-equivalent facts from /proc/cpuinfo + the threading the port uses."""
+    model, phys, logical = "unknown", set(), 0
+    try:
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" not in line:
+                if cur:
+                    phys.add((cur.get("physical id", "0"), cur.get("core id", str(logical))))
+                    cur = {}
+                continue
+            k, v = (x.strip() for x in line.split(":", 1))
+            if k == "processor":
+                logical += 1
+            if k == "model name":
+                model = v
+            if k in ("physical id", "core id"):
+                cur[k] = v
+        if cur:
+            phys.add((cur.get("physical id", "0"), cur.get("core id", str(logical))))
+    except OSError:
+        pass
+    threads = os.cpu_count() or 1
+    return {"cpu_model": model, "logical_cpus": logical or threads, "physical_cores": len(phys) or None,
+            "threading": f"OpenMP gathers (oracle/csrc/gather_ref.c, OMP default = {threads} threads) + "
+                         f"scipy.fft pocketfft workers={threads}; numpy single-threaded elsewhere"}
+
+
+# the reference itself (numba, pkg/src/flowreg) cannot travel to the GPU box
+# (/root/reference is absent there); BASELINE.md §3 measured it in the survey
+# container (1 socket x 8 cores): C1 register 10.1 s, 64^3 matvec 0.341 s,
+# 128^3 near-incompressible matvec 4.36 s.  The port runs C1 in 5.6 s on an
+# 8-core container of the same kind, so GPU / port ratios understate GPU /
+# reference by ~1.8x.
+PORT_VS_NUMBA = {"numba_reference_c1_register_s_8cores": 10.1, "port_c1_register_s_8cores": 5.6,
+                 "source": "BASELINE.md §3 (survey container) and this repo's build container"}
+
+
+def cpu_c1_register():
+    """The oracle port's full C1 solve (64^3 rotation, H1, reg precond, cubic, fd8,
+    f64) on the host cores — BASELINE.md §2 item 3; synth excluded."""
+    from oracle import flowreg_oracle as O
+
+    m0, m1, _ = O.synth_case("rotation", 64, seed=1, d=3, ref_steps=64)
+    t0 = time.perf_counter()
+    _, rep = O.register(m0, m1, O.Reg(alpha=1e-2, incomp="none"), precond="reg", method="cubic", scheme="fd8")
+    dt = time.perf_counter() - t0
+    return {"config": "C1: 64^3 rotation, H1 alpha=1e-2, reg precond, cubic, fd8, f64 (oracle port)",
+            "seconds": dt, "iterations": rep["iterations"], "matvecs": rep["matvecs"],
+            "pde_solves": rep["pde_solves"], "status": rep["status"]}
+
+
 def cpu_baseline(a, m0, m1, vtrue, vt):
-    """Oracle port on the host cores: one full 256^3 matvec (refresh untimed)."""
+    """Oracle port on the host cores: one full 256^3 matvec (refresh untimed)
+    plus a full C1 registration."""
     import numpy as np
 
     from oracle import flowreg_oracle as O
@@ -574,9 +627,11 @@ def cpu_baseline(a, m0, m1, vtrue, vt):
     t0 = time.perf_counter()
     st.hessian_matvec(VT)
     dt = time.perf_counter() - t0
+    del st
     return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"1 Hessian matvec at {a.n}^3 f64 (oracle/flowreg_oracle.py, C/OpenMP gathers + "
-                      f"scipy pocketfft, {cores} threads); refresh excluded"}
+                      f"scipy pocketfft, {cores} threads); refresh excluded",
+            "host": host_info(), "time_to_solution_c1": cpu_c1_register(), "port_vs_numba": PORT_VS_NUMBA}
 
 
 # ---------------------------------------------------------------------------
@@ -608,11 +663,15 @@ def run_reference(a):
     value = steps / dt
     sample = (f"{steps} timed + {warm} warm-up Hessian matvecs at {n}^3 (f64 oracle port, {cores} host threads); "
               f"bounded from --steps {a.steps} --warmup {a.warmup} to keep the run within minutes")
+    del st
+    tts = cpu_c1_register()
     res = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": steps,
            "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle synth_case rotation)",
            "config": config(n, "f64"),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                            "host": host_info(), "port_vs_numba": PORT_VS_NUMBA},
+           "time_to_solution": tts,
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res))
     return res
