@@ -1,4 +1,4 @@
-// Periodic cubic B-spline prefilter as three separable FIR passes (sm_100a).
+// Periodic cubic B-spline prefilter as three separable passes (sm_100a).
 //
 // The coefficients c of the periodic cubic B-spline interpolant of f solve,
 // along every axis, (c[i-1] + 4 c[i] + c[i+1]) / 6 = f[i] (the spectral symbol
@@ -42,17 +42,48 @@ struct FirK<double> {
 
 template <typename T>
 struct FirTaps {
-    T h[FirK<T>::K + 1];
+    T z, c;  // pole, gain sqrt(3) / (1 - z^n)
 };
 
 template <typename T>
 FirTaps<T> fir_taps(int n) {
-    constexpr int K = FirK<T>::K;
-    const double z = std::sqrt(3.0) - 2.0, s3 = std::sqrt(3.0);
-    const double zn = std::pow(z, n);
+    const double z = std::sqrt(3.0) - 2.0;
     FirTaps<T> t;
-    for (int m = 0; m <= K; ++m) t.h[m] = (T)(s3 * (std::pow(z, m) + std::pow(z, n - m)) / (1.0 - zn));
+    t.z = (T)z;
+    t.c = (T)(std::sqrt(3.0) / (1.0 - std::pow(z, n)));
     return t;
+}
+
+// The Q outputs of one thread from its window win[e] = x[o0 - K + e]:
+//   out[q] = c (sum_{m >= 0} z^m x[q - m] + sum_{m >= 1} z^m x[q + m]),
+// the kernel h[m] = c z^|m| of the periodic inverse (its z^(n - |m|) images
+// are below 1e-10 of the signal for n >= 2K + 2).  Each one-sided sum is a
+// first-order recursion seeded from the K window cells beyond the thread's
+// outputs: 2K + 4 Q FMA-class operations for Q outputs instead of (2K + 1) Q
+// for the direct FIR (the kernels were instruction-bound); the sums reach
+// further than K taps inside the window, so the truncation is <= |z|^(K+1).
+template <typename T, int Q, int K, class Win>
+__device__ __forceinline__ void fir_rec(const Win& win, T z, T c, T (&res)[Q]) {
+    // causal: P[q] = x[q] + z P[q - 1], seeded by Horner over x[-K] .. x[0]
+    T P = win(0);
+#pragma unroll
+    for (int e = 1; e <= K; ++e) P = fma(z, P, win(e));
+    res[0] = P;
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        P = fma(z, P, win(K + q));
+        res[q] = P;
+    }
+    // anticausal: A[q] = z B[q], B[q] = x[q + 1] + z B[q + 1], seeded by
+    // Horner over x[Q - 1 + K] .. x[Q]
+    T B = win(Q - 1 + 2 * K);
+#pragma unroll
+    for (int e = Q - 2 + 2 * K; e >= Q + K; --e) B = fma(z, B, win(e));
+#pragma unroll
+    for (int q = Q - 1; q >= 0; --q) {
+        res[q] = c * fma(z, B, res[q]);
+        B = fma(z, B, win(K + q));
+    }
 }
 
 __device__ __forceinline__ int wrapi(int i, int n) {
@@ -93,17 +124,8 @@ __global__ void __launch_bounds__(32 * ROW_WARPS) k_fir_row(const T* __restrict_
         for (int r = 0; r < LPL; ++r) s[rpad<Q>(lane + 32 * r)] = ld[r];
         __syncwarp();
         const int o0 = lane * Q;  // this lane's Q outputs: s0 + o0 ..
-        T win[W];
-#pragma unroll
-        for (int e = 0; e < W; ++e) win[e] = s[rpad<Q>(o0 + e)];
         T res[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            T acc = taps.h[0] * win[q + K];
-#pragma unroll
-            for (int m = 1; m <= K; ++m) acc = fma(taps.h[m], win[q + K - m] + win[q + K + m], acc);
-            res[q] = acc;
-        }
+        fir_rec<T, Q, K>([&](int e) { return s[rpad<Q>(o0 + e)]; }, taps.z, taps.c, res);
         // outputs back through shared memory so the global stores coalesce
         __syncwarp();
 #pragma unroll
@@ -146,16 +168,12 @@ __global__ void __launch_bounds__(256) k_fir_col(const T* __restrict__ in, T* __
 #pragma unroll
     for (int rep = 0; rep < COL_R; ++rep) {
         const int o0 = (ty + 8 * rep) * Q;
-        T win[W];
-#pragma unroll
-        for (int e = 0; e < W; ++e) win[e] = sm[o0 + e][tx];
+        T res[Q];
+        fir_rec<T, Q, K>([&](int e) { return sm[o0 + e][tx]; }, taps.z, taps.c, res);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            T acc = taps.h[0] * win[q + K];
-#pragma unroll
-            for (int m = 1; m <= K; ++m) acc = fma(taps.h[m], win[q + K - m] + win[q + K + m], acc);
             const int l = l0 + o0 + q;
-            if (l < nl) out[base + (long long)l * lstride + c] = acc;
+            if (l < nl) out[base + (long long)l * lstride + c] = res[q];
         }
     }
 }
