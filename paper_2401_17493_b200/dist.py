@@ -12,9 +12,11 @@ This module is that layer for one node of B200s, one process per GPU:
   (``SlabComm.halo``: NCCL send/recv), W = ceil(max |disp_0|) + 2 for cubic,
   computed once per displacement map and max-reduced over ranks, then the
   fp32 TMA gather kernel runs on the owned planes with h0 = W (no axis-0
-  wrap).  This replaces the reference-free "route every off-rank departure
-  point" scheme by a CFL-bounded halo: the same bytes at the CFL numbers of
-  registration velocities, and no per-point bookkeeping;
+  wrap).  This replaces routing every off-rank departure point by a
+  CFL-bounded halo: 3-5x the bytes of routing on the bench maps
+  (profiles/r02_halo_vs_routing_*.json) but one contiguous send/recv per
+  neighbour, no compaction, count exchange or remote-gather pass
+  (DESIGN.md §8);
 * spectral operators run as batched 2D R2C over the owned planes, a packed
   all-to-all to an axis-1 split, a batched 1D C2C along axis 0, the fused
   pointwise operator with global frequencies, and the inverse chain
