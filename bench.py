@@ -547,7 +547,10 @@ def run_slab(a, F, L, world, rank, local, backend):
                                    "near-incompressible beta=1e-4, SSD",
                        "grid": [n, n, n], "n_t": 4, "interp": "cubic", "precision": "mixed",
                        "parallelism": f"slab along axis 0 x{world} ({'gloo-staged' if staged else 'NCCL'} "
-                                      "all-to-all FFT transposes, ghost-plane send/recv)",
+                                      "all-to-all FFT transposes, " +
+                                      ("off-rank stencil planes read from the owners' CUDA-IPC peer windows "
+                                       "(FRG_SLAB_PEER=1)" if os.environ.get("FRG_SLAB_PEER") == "1"
+                                       else "ghost-plane send/recv") + ")",
                        "halo_planes": halo,
                        "l2": "inputs > L2 (GB-scale working set per matvec, no flush needed)"},
             "e2e": {"value": e2e_steps / t_e2e, "unit": UNIT,

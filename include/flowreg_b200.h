@@ -173,6 +173,22 @@ int frg_kkt_destroy(frg_kkt* k);
 /* Destroyed contexts park their device buffers for the next context (capped
    at FRG_POOL_CAP_MB, default 1/4 of device memory); this frees them all. */
 int frg_release_pool(void);
+/* Peer windows of the slab path without ghost planes (dist.py peer mode; no
+ * reference counterpart — the north star's off-rank departure-point exchange,
+ * PAPER.md:545).  A window holds one rank's owned planes (n_loc) of a gathered
+ * source field (fp32); frg_peer_alloc returns it with its 64-byte CUDA IPC
+ * handle, the other ranks map it with frg_peer_open, and frg_peer_register
+ * gives the library every rank's pointer (peers[rank] == local).  Slab SL
+ * calls (frg_slab_*) with h0 == 0 whose sources are registered windows read
+ * the stencil planes of other ranks straight from their windows (TMA / P2P
+ * loads over NVLink): no ghost-plane exchange and no bound on |disp_0|. */
+int frg_peer_alloc(int64_t bytes, void** ptr, void* handle);
+int frg_peer_free(void* ptr);
+int frg_peer_open(const void* handle, void** ptr);
+int frg_peer_close(void* ptr);
+int frg_peer_register(const void* local, const int32_t n_loc[3], int32_t nranks, int32_t rank,
+                      const void* const* peers);
+int frg_peer_unregister(const void* local);
 int frg_kkt_set_stream(frg_kkt* k, void* stream);
 /* images m0, m1 (N values, dtype) — copied into the context             kkt.py:139-162 */
 /* Interpolation precision of the SL steps of the GN Hessian matvec: 32

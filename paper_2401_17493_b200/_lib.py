@@ -76,6 +76,12 @@ PROTOTYPES = {
     "frg_prolong": [_N3, _I, _P, _P, _P],
     "frg_dot": [_I, _P, _P, _L, _DP, _P],
     "frg_release_pool": [],
+    "frg_peer_alloc": [_L, ctypes.POINTER(_P), _P],
+    "frg_peer_free": [_P],
+    "frg_peer_open": [_P, ctypes.POINTER(_P)],
+    "frg_peer_close": [_P],
+    "frg_peer_register": [_P, _N3, _I, _I, ctypes.POINTER(_P)],
+    "frg_peer_unregister": [_P],
     "frg_norm_inf": [_I, _P, _L, _DP, _P],
     "frg_min_max_sum": [_I, _P, _L, _DP, _P],
     "frg_all_finite": [_I, _P, _L, ctypes.POINTER(ctypes.c_int32), _P],

@@ -360,6 +360,35 @@ int frg_kkt_create(const frg_config* cfg, void* stream, frg_kkt** out) {
     });
 }
 
+int frg_peer_alloc(int64_t bytes, void** ptr, void* handle) {
+    return guard([&] {
+        FRG_REQUIRE(bytes > 0 && ptr && handle, "bad peer_alloc arguments");
+        *ptr = ipc_alloc((size_t)bytes, handle);
+    });
+}
+int frg_peer_free(void* ptr) {
+    return guard([&] { FRG_CUDA(cudaFree(ptr)); });
+}
+int frg_peer_open(const void* handle, void** ptr) {
+    return guard([&] {
+        FRG_REQUIRE(handle && ptr, "bad peer_open arguments");
+        *ptr = ipc_open(handle);
+    });
+}
+int frg_peer_close(void* ptr) {
+    return guard([&] { ipc_close(ptr); });
+}
+int frg_peer_register(const void* local, const int32_t n_loc[3], int32_t nranks, int32_t rank,
+                      const void* const* peers) {
+    return guard([&] {
+        FRG_REQUIRE(local && n_loc && peers, "bad peer_register arguments");
+        peer_register((const float*)local, n_loc[0], n_loc[1], n_loc[2], nranks, rank, (const float* const*)peers);
+    });
+}
+int frg_peer_unregister(const void* local) {
+    return guard([&] { peer_unregister((const float*)local); });
+}
+
 int frg_release_pool(void) {
     return guard([&] { kkt_release_pool(); });
 }
@@ -507,7 +536,8 @@ int frg_kkt_detgrad(frg_kkt* k, double out[3]) {
 static Dims slab_dims(const int32_t n_loc[3], int32_t n0_glob, int32_t h0) {
     FRG_REQUIRE(n_loc != nullptr && n_loc[0] >= 1 && n_loc[1] >= 1 && n_loc[2] >= 1, "bad slab grid");
     FRG_REQUIRE(n0_glob >= n_loc[0] && h0 >= 0, "bad slab decomposition");
-    FRG_REQUIRE(h0 >= 1, "slab sources carry at least one ghost plane");
+    // h0 == 0: the sources are peer windows (frg_peer_register), planes off
+    // the slab are read from the owning rank over NVLink
     Dims g = make_dims(n_loc, 3);
     g.h0 = h0;
     g.n0g = n0_glob;

@@ -86,8 +86,17 @@ __device__ __forceinline__ void fir_rec(const Win& win, T z, T c, T (&res)[Q]) {
     }
 }
 
-// periodic index for i in [-n, 2n) (halo offsets are < K < n): two selects, no division
+// periodic index: one compare in range, a division only for indices outside
+// [0, n) (a column tile of 8 Q R + 2K rows can exceed a short axis)
 __device__ __forceinline__ int wrapi(int i, int n) {
+    if ((unsigned)i >= (unsigned)n) {
+        i %= n;
+        i = i < 0 ? i + n : i;
+    }
+    return i;
+}
+// the same for i in [-n, 2n) (every axis at least as long as the tile + halo)
+__device__ __forceinline__ int wrap1(int i, int n) {
     i = i < 0 ? i + n : i;
     return i >= n ? i - n : i;
 }
@@ -119,7 +128,10 @@ __global__ void __launch_bounds__(32 * ROW_WARPS) k_fir_row(const T* __restrict_
         static_assert((ROW_SEG + 2 * K) % 32 == 0, "row segment + halo must be whole warps");
         T ld[LPL];
 #pragma unroll
-        for (int r = 0; r < LPL; ++r) ld[r] = __ldg(src + wrapi(s0 - K + lane + 32 * r, n2));
+        for (int r = 0; r < LPL; ++r) {
+            const int e = s0 - K + lane + 32 * r;
+            ld[r] = __ldg(src + (n2 >= ROW_SEG + K ? wrap1(e, n2) : wrapi(e, n2)));
+        }
 #pragma unroll
         for (int r = 0; r < LPL; ++r) s[rpad<Q>(lane + 32 * r)] = ld[r];
         __syncwarp();
@@ -161,7 +173,10 @@ __global__ void __launch_bounds__(256) k_fir_col(const T* __restrict__ in, T* __
         const T* __restrict__ src = in + base + c;
         T ld[ROWS / 8];
 #pragma unroll
-        for (int r = 0; r < ROWS / 8; ++r) ld[r] = __ldg(src + wrapi(l0 - K + ty + 8 * r, nl) * ls);
+        for (int r = 0; r < ROWS / 8; ++r) {
+            const int e = l0 - K + ty + 8 * r;
+            ld[r] = __ldg(src + (nl >= COL_SEG + K ? wrap1(e, nl) : wrapi(e, nl)) * ls);
+        }
 #pragma unroll
         for (int r = 0; r < ROWS / 8; ++r) sm[ty + 8 * r][tx] = ld[r];
     }

@@ -155,4 +155,11 @@ double slab_grad_energy(const Dims& g, int i1_off, int n1_loc, const void* x_spe
 void slab_spec_combine(const Dims& g, int i1_off, int n1_loc, int dtype, void* a, const void* b, const RegSpec& r,
                        bool project, cudaStream_t st);
 
+// peer windows of the slab path without ghost planes (tma.cu)
+void peer_register(const float* local, int n0, int n1, int n2, int nranks, int rank, const float* const* peers);
+void peer_unregister(const float* local);
+void* ipc_alloc(size_t bytes, void* handle);
+void* ipc_open(const void* handle);
+void ipc_close(void* p);
+
 }  // namespace frg

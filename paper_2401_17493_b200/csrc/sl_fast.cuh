@@ -105,6 +105,71 @@ __device__ __forceinline__ void tma_box(float* box, const CUtensorMap* map, cons
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+// ---------------------------------------------------------------------------
+// Off-rank planes over NVLink peer memory (slab mode without ghost planes,
+// dist.py peer mode).  Each rank exposes its owned planes of a gathered
+// source in a window buffer mapped into every other rank (CUDA IPC); a plane
+// index b of the local slab that falls outside [0, n0) is read from the rank
+// that owns global plane rank * n0 + b — by TMA (one device-resident tensor
+// map per rank and field) into the box, or by P2P loads in the per-voxel
+// fallback and the periodic patches.  Exactly the stencil planes a tile needs
+// cross NVLink, with no ghost-plane exchange and no limit on |disp_0|.
+constexpr int PEER_MAX = 8;
+struct PeerPlanes {
+    int nranks = 0;  // 0: not in peer mode
+    int rank = 0;
+    const CUtensorMap* maps[3] = {nullptr, nullptr, nullptr};  // per field: nranks maps, rank r's window
+    const float* base[3][PEER_MAX] = {};                       // per field, per rank: window base
+};
+// owner rank and its local plane of local plane index b (|b| < n0g)
+__device__ __forceinline__ void peer_plane(const Dims& g, const PeerPlanes& pp, int b, int& owner, int& local) {
+    int G = pp.rank * g.n0 + b;
+    G = G < 0 ? G + g.n0g : (G >= g.n0g ? G - g.n0g : G);
+    owner = G / g.n0;
+    local = G - owner * g.n0;
+}
+__device__ __forceinline__ const float* peer_plane_ptr(const Dims& g, const PeerPlanes& pp, int f, int b) {
+    int o, l;
+    peer_plane(g, pp, b, o, l);
+    return pp.base[f][o] + (size_t)l * g.n1 * g.n2;
+}
+template <int PLANE = TB_PLANE>
+__device__ __forceinline__ void tma_box_peer(float* box, const PeerPlanes& pp, int f, const Dims& g, int lo0, int lo1,
+                                             int lo2, int S0, uint64_t* bar) {
+    mbar_expect_tx(bar, (unsigned)(S0 * PLANE * sizeof(float)));
+    for (int a = 0; a < S0; ++a) {
+        int o, l;
+        peer_plane(g, pp, lo0 + a, o, l);
+        tma_load_2d(box + a * PLANE, pp.maps[f] + o, lo2, l * g.n1 + lo1, bar);
+    }
+}
+// per-voxel stencil with axis-0 planes resolved through the peer windows
+template <int M>
+__device__ __forceinline__ float peer_interp(const Dims& g, const PeerPlanes& pp, int f, int b0, int b1, int b2,
+                                             float t0, float t1, float t2) {
+    constexpr int NT = Taps<M>::value;
+    Axis<float, NT> a0, a1, a2;
+    axis_stencil<float, M>(0, t0, 1 << 30, 0, a0);  // weights only (no wrap along axis 0)
+    axis_stencil<float, M>(b1, t1, g.n1, g.n2, a1);
+    axis_stencil<float, M>(b2, t2, g.n2, 1, a2);
+    const int first = b0 - Halo<M>::lo;
+    float acc = 0.f;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) {
+        const float* __restrict__ pl = peer_plane_ptr(g, pp, f, first + a);
+        float plane = 0.f;
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+            float row = 0.f;
+#pragma unroll
+            for (int c = 0; c < NT; ++c) row = fmaf(a2.w[c], __ldg(pl + a1.off[b] + a2.off[c]), row);
+            plane = fmaf(a1.w[b], row, plane);
+        }
+        acc = fmaf(a0.w[a], plane, acc);
+    }
+    return acc;
+}
+
 // Lagrange cubic weights (nodes -1, 0, 1, 2; _kernels.py:162-167) in 3 FADD +
 // 10 FMUL: the shared products t(t-1) and (t+1)(t-2) are formed once.
 __device__ __forceinline__ void lagrange4f(float t, float (&w)[4]) {
@@ -150,10 +215,10 @@ __device__ __forceinline__ float linear_fixed(const float* __restrict__ b, float
 
 // copy the box elements whose coordinate along `axis` leaves [0, n) from their
 // periodic images (after the TMA zero-filled them); 4-byte cp.async
-template <int J = TB_J, int K = TB_K>
-__device__ __forceinline__ void patch_axis(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
-                                           int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid,
-                                           int nthreads = BX * BY) {
+template <int J = TB_J, int K = TB_K, class PlaneOf>
+__device__ __forceinline__ void patch_axis_f(float* __restrict__ box, const PlaneOf& plane_of, const Dims& g,
+                                             int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid,
+                                             int nthreads) {
     const int lo = axis == 0 ? lo0 : (axis == 1 ? lo1 : lo2);
     const int S = axis == 0 ? S0 : (axis == 1 ? S1 : S2);
     const int n = g.axis_len(axis);
@@ -180,9 +245,17 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
         } else {
             a = in1; b = in2; c = x;
         }
-        const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
-        cp_async_elem<4>(box + (a * J + b) * K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
+        const int gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        cp_async_elem<4>(box + (a * J + b) * K + c, plane_of(lo0 + a) + (gj * g.n2 + gk));
     }
+}
+template <int J = TB_J, int K = TB_K>
+__device__ __forceinline__ void patch_axis(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
+                                           int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid,
+                                           int nthreads = BX * BY) {
+    const size_t plane = (size_t)g.n1 * g.n2;
+    patch_axis_f<J, K>(box, [&](int b) { return src + src_plane(g, b) * plane; }, g, lo0, lo1, lo2, S0, S1, S2, axis,
+                       tid, nthreads);
 }
 
 // whole-box cp.async staging with wrap (grids smaller than the TMA box)
@@ -373,7 +446,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 
 template <int M, int NF, class Op>
 __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
-    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma) {
+    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma, const __grid_constant__ PeerPlanes pp) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
     extern __shared__ __align__(16) unsigned char sdyn[];
@@ -430,7 +503,12 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         S1 = (pe.w >> 10) & 1023;
         S2 = (pe.w >> 20) & 1023;
         if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
-            for (int b = 0; b < NB; ++b) tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
+            for (int b = 0; b < NB; ++b) {
+                if (pp.nranks)
+                    tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
+                else
+                    tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
+            }
         // no CTA barrier here: the other warps go on with their displacement
         // arithmetic while thread 0 waits for the plan entry and issues the TMA
     }
@@ -488,7 +566,12 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     S1 = mx1 + Halo<M>::hi - lo1 + 1;
     S2 = mx2 + Halo<M>::hi - lo2 + 1;
     if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
-        for (int b = 0; b < NB; ++b) tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
+        for (int b = 0; b < NB; ++b) {
+            if (pp.nranks)
+                tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
+            else
+                tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
+        }
     }
     const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
 
@@ -511,8 +594,14 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
             if (use_tma) {
                 mbar_wait_sleep(&bars[f % NB], (unsigned)((f / NB) & 1));
                 if (wrap) {  // planes already wrapped by tma_box
-                    patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
-                    patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
+                    if (pp.nranks) {
+                        auto of = [&](int b) { return peer_plane_ptr(g, pp, f, b); };
+                        patch_axis_f<TB_J, TB_K>(box, of, g, lo0, lo1, lo2, S0, S1, S2, 1, tid, BX * BY);
+                        patch_axis_f<TB_J, TB_K>(box, of, g, lo0, lo1, lo2, S0, S1, S2, 2, tid, BX * BY);
+                    } else {
+                        patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 1, tid);
+                        patch_axis(box, src, g, lo0, lo1, lo2, S0, S1, S2, 2, tid);
+                    }
                     cp_async_wait_all();
                     __syncthreads();
                 }
@@ -541,7 +630,10 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
                 __syncthreads();  // every thread is done reading this buffer
                 if (tid == 0) {
                     fence_proxy_async();
-                    tma_box(box, &maps.m[f + NB], g, lo0, lo1, lo2, S0, &bars[f % NB]);
+                    if (pp.nranks)
+                        tma_box_peer(box, pp, f + NB, g, lo0, lo1, lo2, S0, &bars[f % NB]);
+                    else
+                        tma_box(box, &maps.m[f + NB], g, lo0, lo1, lo2, S0, &bars[f % NB]);
                 }
             }
         }
@@ -554,9 +646,10 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
             const float* src = op.field(f);
 #pragma unroll
             for (int u = 0; u < SL_TI; ++u)
-                vals[u][f] = ok[u] ? global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u], base2[u],
-                                                                    fr0[u], fr1[u], fr2[u])
-                                   : 0.f;
+                vals[u][f] = !ok[u]      ? 0.f
+                             : pp.nranks ? peer_interp<M>(g, pp, f, base0[u], base1[u], base2[u], fr0[u], fr1[u], fr2[u])
+                                         : global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u],
+                                                                          base2[u], fr0[u], fr1[u], fr2[u]);
         }
     }
     if constexpr (HasTileSmem<Op>::value) {
@@ -590,15 +683,24 @@ inline size_t tile_plan_count(const Dims& g) {
     return (size_t)gr.x * gr.y * gr.z;
 }
 
+// host: peer windows registered by frg_peer_register (tma.cu); fills pp for
+// the launch's source fields, false when field 0 is not a registered window
+bool peer_planes_of(const Dims& g, const float* const* fields, int nf, PeerPlanes& pp);
+
 template <int M, int NF, class Op>
 void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
     Op op = op_in;
     if constexpr (HasDs<Op>::value)
         if (op.ds.plan && plan_method(op.ds.plan) != M) op.ds.plan = nullptr;
     TmaMaps<NF> maps;
-    const int use_tma = tma_grid_ok(g) ? 1 : 0;
+    PeerPlanes pp;
+    const float* fields[NF];
+    for (int f = 0; f < NF; ++f) fields[f] = op.field(f);
+    const bool peer = g.n0g > 0 && g.h0 == 0 && peer_planes_of(g, fields, NF, pp);
+    FRG_REQUIRE(peer || g.n0g == 0 || g.h0 > 0, "slab gathers without ghost planes need registered peer windows");
+    const int use_tma = (peer || tma_grid_ok(g)) ? 1 : 0;
     for (int f = 0; f < NF; ++f) {
-        if (use_tma)
+        if (use_tma && !peer)
             encode_field_map(&maps.m[f], op.field(f), g);
         else
             memset(&maps.m[f], 0, sizeof(CUtensorMap));
@@ -609,7 +711,7 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
         FRG_CUDA(cudaFuncSetAttribute(k_slf<M, NF, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
-    k_slf<M, NF, Op><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma);
+    k_slf<M, NF, Op><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, pp);
     FRG_CHECK_LAUNCH();
 }
 

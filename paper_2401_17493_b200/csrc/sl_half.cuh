@@ -296,7 +296,7 @@ void* bspline_scratch(int slot, size_t bytes);
 template <typename T, int NF, class Op>
 void launch_sl(const Dims& g, int method, const Op& op_in, cudaStream_t st) {
     Op op = op_in;
-    if (method == BSPLINE && g.h0 == 0) {
+    if (method == BSPLINE && g.h0 == 0 && g.n0g == 0) {  // slab sources (ghosted or peer windows) are coefficients
         using V = typename Op::V;
         for (int f = 0; f < NF; ++f) {
             V* c = (V*)bspline_scratch(f, sizeof(V) * (size_t)g.N);

@@ -3,7 +3,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <array>
+#include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "sl_half.cuh"
 
@@ -114,6 +117,106 @@ void* bspline_scratch(int slot, size_t bytes) {
         s.cap = bytes;
     }
     return s.p;
+}
+
+// ---------------------------------------------------------------------------
+// Peer windows (dist.py peer mode): device buffers exported to / imported from
+// the other ranks with CUDA IPC, and per local window the tensor maps of every
+// rank's copy (device-resident: k_slf reads them by address).
+namespace {
+struct PeerWin {
+    int n0, n1, n2, nranks, rank;
+    CUtensorMap* dev_maps;
+    const float* peer[PEER_MAX];
+};
+std::mutex g_peer_mu;
+std::unordered_map<const void*, PeerWin>& peer_wins() {
+    static std::unordered_map<const void*, PeerWin> m;
+    return m;
+}
+std::unordered_map<void*, void*>& ipc_opened() {  // mapped pointer -> IPC base
+    static std::unordered_map<void*, void*> m;
+    return m;
+}
+}  // namespace
+
+void peer_register(const float* local, int n0, int n1, int n2, int nranks, int rank, const float* const* peers) {
+    FRG_REQUIRE(nranks >= 1 && nranks <= PEER_MAX && rank >= 0 && rank < nranks, "peer windows: 1..8 ranks");
+    FRG_REQUIRE(n1 >= TB_J && n2 >= TB_K && n2 % 4 == 0, "peer windows need n1 >= 16, n2 >= 64, n2 % 4 == 0");
+    FRG_REQUIRE(peers[rank] == local, "peer windows: this rank's entry must be the local window");
+    CUtensorMap h[PEER_MAX];
+    Dims w = make_dims(std::array<int32_t, 3>{n0, n1, n2}.data(), 3);
+    for (int r = 0; r < nranks; ++r) encode_field_map(&h[r], peers[r], w);
+    PeerWin e;
+    e.n0 = n0;
+    e.n1 = n1;
+    e.n2 = n2;
+    e.nranks = nranks;
+    e.rank = rank;
+    for (int r = 0; r < PEER_MAX; ++r) e.peer[r] = r < nranks ? peers[r] : nullptr;
+    FRG_CUDA(cudaMalloc(&e.dev_maps, sizeof(CUtensorMap) * nranks));
+    FRG_CUDA(cudaMemcpy(e.dev_maps, h, sizeof(CUtensorMap) * nranks, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    auto it = peer_wins().find(local);
+    if (it != peer_wins().end()) {
+        cudaFree(it->second.dev_maps);
+        peer_wins().erase(it);
+    }
+    peer_wins()[local] = e;
+}
+
+void peer_unregister(const float* local) {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    auto it = peer_wins().find(local);
+    if (it == peer_wins().end()) return;
+    cudaFree(it->second.dev_maps);
+    peer_wins().erase(it);
+}
+
+bool peer_planes_of(const Dims& g, const float* const* fields, int nf, PeerPlanes& pp) {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    if (peer_wins().empty()) return false;
+    FRG_REQUIRE(nf <= 3, "peer gathers take at most 3 fields");
+    for (int f = 0; f < nf; ++f) {
+        auto it = peer_wins().find(fields[f]);
+        if (it == peer_wins().end()) {
+            FRG_REQUIRE(f == 0, "peer gather: every source must be a registered window");
+            return false;
+        }
+        const PeerWin& e = it->second;
+        FRG_REQUIRE(e.n0 == g.n0 && e.n1 == g.n1 && e.n2 == g.n2 && e.nranks * g.n0 == g.n0g,
+                    "peer window does not match the slab grid");
+        pp.nranks = e.nranks;
+        pp.rank = e.rank;
+        pp.maps[f] = e.dev_maps;
+        for (int r = 0; r < PEER_MAX; ++r) pp.base[f][r] = e.peer[r];
+    }
+    return true;
+}
+
+void* ipc_alloc(size_t bytes, void* handle) {
+    void* p = nullptr;
+    FRG_CUDA(cudaMalloc(&p, bytes));
+    FRG_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), p));
+    return p;
+}
+
+void* ipc_open(const void* handle) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    FRG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    ipc_opened()[p] = p;
+    return p;
+}
+
+void ipc_close(void* p) {
+    {
+        std::lock_guard<std::mutex> lk(g_peer_mu);
+        ipc_opened().erase(p);
+    }
+    FRG_CUDA(cudaIpcCloseMemHandle(p));
 }
 
 }  // namespace frg

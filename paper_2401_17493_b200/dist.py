@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -103,6 +104,20 @@ class SlabComm:
         else:
             tdist.all_to_all_single(out, inp, group=self.group)
 
+    def device_barrier(self) -> None:
+        """Order every rank's prior device work before every rank's next
+        kernel: a one-element NCCL all-reduce on the current stream (gloo:
+        synchronise the device, then a host barrier)."""
+        if self.size == 1:
+            return
+        if self.staged:
+            torch.cuda.synchronize()
+            tdist.barrier(group=self.group)
+            return
+        if getattr(self, "_bar", None) is None:
+            self._bar = torch.zeros(1, dtype=torch.float32, device="cuda")
+        tdist.all_reduce(self._bar, group=self.group)
+
     # -- ghost planes ----------------------------------------------------
     def halo(self, ext: torch.Tensor, W: int) -> None:
         """ext (C, n0_loc + 2W, n1, n2) with the owned planes at [W, W + n0_loc):
@@ -135,6 +150,104 @@ class SlabComm:
             req.wait()
         ext[:, :W].copy_(recv_lo)
         ext[:, n0l + W:].copy_(recv_hi)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ of a raw fp32 device buffer (torch.as_tensor wraps it, zero copy)."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 2}
+
+
+class PeerWindows:
+    """Peer mode of the slab path (no ghost planes): NBLK blocks of
+    (C, n0_loc, n1, n2) fp32 per rank, exported with CUDA IPC, mapped into
+    every other rank and registered per component with the library
+    (frg_peer_register), so that a slab SL call whose sources are window
+    components reads the stencil planes owned by other ranks straight from
+    their windows — TMA / P2P loads over NVLink — instead of exchanging
+    CFL-wide ghost slabs (the north star's off-rank departure points,
+    PAPER.md:545).  Blocks alternate between gathers: one device barrier per
+    gather (after filling the next block) orders every rank's fill before
+    every peer's reads and every peer's reads of a block before its refill."""
+
+    NBLK = 2
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, comm: SlabComm, shape) -> "PeerWindows":
+        """One set of windows per (communicator, shape) for the life of the
+        process: freeing a window while a peer may still read it would need a
+        collective in a destructor; states of the same grid share the ring."""
+        key = (id(comm.group), comm.rank, comm.size, tuple(int(x) for x in shape))
+        w = cls._cache.get(key)
+        if w is None:
+            w = cls._cache[key] = cls(comm, shape)
+        else:
+            w.comm = comm
+        return w
+
+    def __init__(self, comm: SlabComm, shape):
+        self.comm, self.shape = comm, tuple(int(x) for x in shape)
+        P, rank = comm.size, comm.rank
+        C = self.shape[0]
+        comp = int(np.prod(self.shape[1:]))
+        self._own, self._opened, self.blocks = [], [], []
+        n3 = L.n3(self.shape[1:])
+        for _ in range(self.NBLK):
+            ptr, h = ctypes.c_void_p(), (ctypes.c_ubyte * 64)()
+            L.check(L.lib().frg_peer_alloc(4 * C * comp, ctypes.byref(ptr), h), "peer_alloc")
+            self._own.append(ptr.value)
+            handles = [None] * P
+            tdist.all_gather_object(handles, bytes(h), group=comm.group)
+            bases = []
+            for r in range(P):
+                if r == rank:
+                    bases.append(ptr.value)
+                    continue
+                q = ctypes.c_void_p()
+                hb = (ctypes.c_ubyte * 64).from_buffer_copy(handles[r])
+                L.check(L.lib().frg_peer_open(hb, ctypes.byref(q)), "peer_open")
+                self._opened.append(q.value)
+                bases.append(q.value)
+            for c in range(C):
+                off = 4 * c * comp
+                arr = (ctypes.c_void_p * P)(*[b + off for b in bases])
+                L.check(L.lib().frg_peer_register(ctypes.c_void_p(ptr.value + off), n3, P, rank, arr),
+                        "peer_register")
+            self.blocks.append(torch.as_tensor(_CudaArray(ptr.value, self.shape), device="cuda"))
+        self._k = 0
+        comm.device_barrier()
+
+    def next(self, C: int) -> torch.Tensor:
+        """The next block's first C components (the caller fills them, then calls publish())."""
+        if C > self.shape[0]:
+            raise ValueError(f"{C} fields exceed the {self.shape[0]}-component peer windows")
+        blk = self.blocks[self._k % self.NBLK]
+        self._k += 1
+        return blk[:C]
+
+    def publish(self) -> None:
+        self.comm.device_barrier()
+
+    def close(self):
+        lib = L._lib
+        if lib is None:
+            return
+        try:
+            torch.cuda.synchronize()
+            comp = int(np.prod(self.shape[1:]))
+            for p in self._own:
+                for c in range(self.shape[0]):
+                    lib.frg_peer_unregister(ctypes.c_void_p(p + 4 * c * comp))
+            for q in self._opened:
+                lib.frg_peer_close(ctypes.c_void_p(q))
+            for p in self._own:
+                lib.frg_peer_free(ctypes.c_void_p(p))
+        except Exception:
+            pass
+        self._own, self._opened = [], []
 
 
 @dataclass(frozen=True)
@@ -284,11 +397,17 @@ class DistKktState:
     of per-rank slab kernels and exchanges; all ranks call them in lockstep."""
 
     def __init__(self, m0: torch.Tensor, m1: torch.Tensor, reg: RegConfig, comm: SlabComm, n_glob, n_t: int = 4,
-                 method: str = "cubic", v_init: torch.Tensor | None = None):
+                 method: str = "cubic", v_init: torch.Tensor | None = None, peer: bool | None = None):
+        """``peer=True`` (default: env FRG_SLAB_PEER=1): SL gathers read off-rank
+        stencil planes from the owners' peer windows (PeerWindows) instead of
+        exchanging ghost slabs of width ceil(max |disp_0|) + 2; FD8 keeps its
+        4 ghost planes."""
         if method not in ("linear", "cubic", "bspline"):
             raise ValueError("slab transport supports linear / cubic / bspline interpolation")
         self.comm = comm
         self.grid = SlabGrid(tuple(int(v) for v in n_glob), comm.rank, comm.size, n_t=n_t)
+        self.peer = (os.environ.get("FRG_SLAB_PEER") == "1") if peer is None else bool(peer)
+        self._win = PeerWindows.get(comm, (9, *self.grid.n)) if self.peer else None
         self.reg = reg
         self.method = method
         self._m = L.METHODS[method]
@@ -333,7 +452,15 @@ class DistKktState:
         return self.fft.apply(xx.contiguous(), "bspline_prefilter", self._reg).view(x.shape)
 
     def _src(self, x: torch.Tensor, W: int) -> torch.Tensor:
-        """Ghost-extended gather source of x (coefficients for B-spline)."""
+        """Ghost-extended gather source of x (coefficients for B-spline); in
+        peer mode (W == 0) the next published peer-window block."""
+        if self.peer:
+            c = self._coef(x)
+            c = c if c.dim() == 4 else c.unsqueeze(0)
+            blk = self._win.next(c.shape[0])
+            blk.copy_(c)
+            self._win.publish()
+            return blk
         return self._ext(self._coef(x), W)
 
     def _plan(self, disp: torch.Tensor) -> torch.Tensor:
@@ -365,6 +492,8 @@ class DistKktState:
         return self.comm.all_reduce(out.value, "max")
 
     def _halo_of(self, disp: torch.Tensor) -> int:
+        if self.peer:
+            return 0
         return max(halo_width(self._absmax(disp[0]), self.method), 1)
 
     def dot(self, a: torch.Tensor, b: torch.Tensor) -> float:
@@ -393,7 +522,7 @@ class DistKktState:
     def _departure(self, v32: torch.Tensor, sign: float) -> torch.Tensor:
         vs = v32 if sign > 0 else -v32
         h0 = TWO_PI / self.grid.n_glob[0]
-        Wv = max(halo_width(self._absmax(v32[0]) * self.grid.h_t / h0, self.method), 4)
+        Wv = 0 if self.peer else max(halo_width(self._absmax(v32[0]) * self.grid.h_t / h0, self.method), 4)
         v_ext = self._src(vs, Wv)
         disp = torch.empty_like(vs)
         L.check(L.lib().frg_slab_departure(self.n_loc, self.grid.n_glob[0], Wv, self._m, self.grid.h_t, _c(v_ext),
@@ -447,7 +576,8 @@ class DistKktState:
         self._bind()
         divv = torch.empty(g.n, dtype=torch.float32, device="cuda")
         self.divv = divv
-        if self._bs:  # the departure solve exchanged coefficients; FD8 needs the nodal values
+        if self._bs or self.peer:  # FD8 needs the nodal values with >= 4 ghost planes
+            Wv = max(Wv, 4)
             v_ext = self._ext(v32, Wv)
         L.check(L.lib().frg_slab_fd8_divergence(self.n_loc, g.n_glob[0], Wv, _c(v_ext), _c(divv), L.stream()),
                 "slab_fd8_divergence")
@@ -497,12 +627,16 @@ class DistKktState:
             vt_loc = vt.to(torch.float32).contiguous()
             vt_ext, vt_loc_p = self._src(vt_loc, Wf), _c(vt_loc)
         else:
-            vt_ext = torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
+            vt_ext = (self._win.next(3) if self.peer else
+                      torch.empty((3, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda"))
             vt64 = vt.to(torch.float64).contiguous()
             for c in range(3):  # f64 -> f32 straight into the owned planes (vectorised convert)
                 L.check(L.lib().frg_convert(L.F64, _c(vt64[c]), L.F32, _c(vt_ext[c, Wf:Wf + n0l]), self.N,
                                             L.stream()), "convert")
-            self.comm.halo(vt_ext, Wf)
+            if self.peer:
+                self._win.publish()
+            else:
+                self.comm.halo(vt_ext, Wf)
             vt_loc_p = None
         mt = torch.empty((g.n_t + 1, n0l + 2 * Wf, *g.n[1:]), dtype=torch.float32, device="cuda")
         S = torch.empty((max(g.n_t - 1, 1), *g.n), dtype=torch.float32, device="cuda")
@@ -512,8 +646,8 @@ class DistKktState:
                                            _c(S), L.stream()), "slab_inc_first")
 
         def source(series, j, W):  # ghost-extended gather source of slice j
-            if self._bs:
-                return self._src(series[j, W:W + n0l], W)
+            if self._bs or self.peer:
+                return self._src(series[j, W:W + n0l], W)[0]
             self.comm.halo(series[j:j + 1], W)
             return series[j]
 

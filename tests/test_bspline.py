@@ -96,7 +96,9 @@ def test_bspline_registration_converges():
 @pytest.mark.parametrize("shape,dtype,tol", [((72, 68, 80), np.float64, 1e-12), ((40, 48, 64), np.float32, 1e-5),
                                              ((40, 96), np.float32, 1e-5),
                                              # fused axes-2+1 kernel (n2 in {128, 256, 512}, n1 % 32 == 0)
-                                             ((36, 64, 128), np.float32, 1e-5), ((34, 32, 256), np.float32, 1e-5)])
+                                             ((36, 64, 128), np.float32, 1e-5), ((34, 32, 256), np.float32, 1e-5),
+                                             # axes shorter than a column tile (8 Q R + 2K rows)
+                                             ((64, 64, 64), np.float32, 1e-5)])
 def test_fir_prefilter_matches_oracle(shape, dtype, tol):
     """Grids whose axes are all >= 2K + 2 take the separable FIR prefilter
     (csrc/bspline.cu) instead of the spectral round trip: same interpolant

@@ -39,9 +39,11 @@ def _rel(a, b):
     return float((a - b).norm() / max(float(b.norm()), 1e-300))
 
 
-def _worker(rank, size, port, n, outdir, do_register, method):
+def _worker(rank, size, port, n, outdir, do_register, method, peer=False):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if peer:  # slab gathers read off-rank planes from the owners' IPC windows (dist.PeerWindows)
+        os.environ["FRG_SLAB_PEER"] = "1"
     import torch.distributed as tdist
 
     torch.cuda.set_device(0)
@@ -120,10 +122,10 @@ def _worker(rank, size, port, n, outdir, do_register, method):
     tdist.destroy_process_group()
 
 
-def _run(size, n, tmp_path, do_register=False, method="cubic"):
+def _run(size, n, tmp_path, do_register=False, method="cubic", peer=False):
     import torch.multiprocessing as mp
 
-    mp.start_processes(_worker, args=(size, _free_port(), n, str(tmp_path), do_register, method), nprocs=size,
+    mp.start_processes(_worker, args=(size, _free_port(), n, str(tmp_path), do_register, method, peer), nprocs=size,
                        start_method="spawn", join=True)
     return [json.load(open(os.path.join(tmp_path, f"rank{r}.json"))) for r in range(size)]
 
@@ -137,6 +139,74 @@ def test_slab_kkt_matches_single_gpu(size, tmp_path):
         assert res["mismatch"] < 1e-6, res
         de, de1 = res["divergence_energy"]  # kkt.py:207-218 (near-incompressible)
         assert de1 > 0 and abs(de - de1) < 1e-6 * de1, res
+
+
+@pytest.mark.parametrize("size,method", [(2, "cubic"), (4, "cubic"), (2, "bspline")])
+def test_slab_peer_mode_matches_single_gpu(size, method, tmp_path):
+    """Peer mode (no ghost planes): off-rank stencil planes come from the
+    owners' CUDA-IPC windows by TMA / P2P loads; same bars as the halo mode."""
+    for rank, res in enumerate(_run(size, 64, tmp_path, method=method, peer=True)):
+        for key in ("gradient", "matvec", "precond"):
+            assert res[key] < 1e-5, (size, method, rank, key, res[key])
+        assert res["objective"] < 1e-6 and res["objective_at"] < 1e-6, res
+        assert res["mismatch"] < 1e-6, res
+
+
+def _worker_far(rank, size, port, n, outdir, shift):
+    """Displacements along axis 0 larger than a slab: the halo mode cannot
+    run (W > slab thickness), the peer mode reads the departure points'
+    planes from ranks that are not neighbours."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=size)
+    import paper_2401_17493_b200 as F
+    from paper_2401_17493_b200 import dist as D
+
+    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3)
+    reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    v = 0.5 * vtrue.data.clone()
+    v[0] += shift  # |disp_0| = shift * h_t / h_0 cells per step
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    vt = 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=torch.float64, device="cuda")
+    ref = F.KktState(m0, m1, reg, v_init=F.VectorField._wrap(m0.grid, v), transport_dtype=np.float32)
+    comm = D.SlabComm()
+    lo, hi = D.slab_bounds(n, size, rank)
+    res = {}
+    try:
+        D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
+                       v_init=v[:, lo:hi].contiguous(), peer=False)
+        res["halo_ran"] = True
+    except ValueError:
+        res["halo_ran"] = False
+    st = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
+                        v_init=v[:, lo:hi].contiguous(), peer=True)
+    res["max_disp0"] = st._absmax(st.disp_f[0])
+    res["gradient"] = _rel(st.gradient().data, ref.gradient().data[:, lo:hi])
+    res["matvec"] = _rel(st.hessian_matvec(vt[:, lo:hi].contiguous()).data,
+                         ref.hessian_matvec(F.VectorField._wrap(m0.grid, vt)).data[:, lo:hi])
+    res["objective"] = abs(st.objective() - ref.objective()) / abs(ref.objective())
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as fh:
+        json.dump(res, fh)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_slab_peer_mode_reaches_past_the_slab(tmp_path):
+    import torch.multiprocessing as mp
+
+    size, n = 4, 64  # 16-plane slabs; a shift of 7 (rad / unit time) moves ~18 planes per step
+    mp.start_processes(_worker_far, args=(size, _free_port(), n, str(tmp_path), 7.0), nprocs=size,
+                       start_method="spawn", join=True)
+    for r in range(size):
+        res = json.load(open(os.path.join(tmp_path, f"rank{r}.json")))
+        assert res["max_disp0"] > n // size, res
+        assert res["halo_ran"] is False, res
+        for key in ("gradient", "matvec"):
+            assert res[key] < 1e-5, (r, key, res[key])
+        assert res["objective"] < 1e-6, res
 
 
 @pytest.mark.parametrize("method", ["bspline", "linear"])
