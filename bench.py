@@ -476,7 +476,7 @@ def run_slab(a, F, L, world, rank, local, backend):
 
     # dominant kernel: one planned single-field SL gather step on this rank's slab
     src = torch.randn((1, n0l, n, n), generator=gen, dtype=torch.float32, device="cuda")
-    ext = st._ext(src, st.Wf)
+    ext = st._src(src, st.Wf)  # ghost-extended, or (peer mode) a published peer window
     g_out = torch.empty((n0l, n, n), dtype=torch.float32, device="cuda")
     st._bind()
     for _ in range(3):

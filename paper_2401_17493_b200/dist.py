@@ -864,6 +864,8 @@ class _SlabTransport(DistKktState):
         self.fft = SlabFFT(self.grid, comm)
         self.n_loc = L.n3(self.grid.n)
         self.N = int(np.prod(self.grid.n))
+        self.peer = os.environ.get("FRG_SLAB_PEER") == "1"
+        self._win = PeerWindows.get(comm, (9, *self.grid.n)) if self.peer else None
 
 
 def slab_synth(name: str, n: int, comm: SlabComm, seed: int = 1, amp: float = 0.7, ref_steps: int = 64):

@@ -251,7 +251,9 @@ def test_slab_search_alpha_matches_single_gpu(tmp_path):
             assert np.allclose(a, b, rtol=1e-4, atol=1e-6), (a, b)
 
 
-def _synth_worker(rank, size, port, n, outdir):
+def _synth_worker(rank, size, port, n, outdir, peer=False):
+    if peer:
+        os.environ["FRG_SLAB_PEER"] = "1"
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as tdist
@@ -271,14 +273,15 @@ def _synth_worker(rank, size, port, n, outdir):
     tdist.destroy_process_group()
 
 
-def test_slab_synth_matches_single_gpu_generator(tmp_path):
+@pytest.mark.parametrize("peer", [False, True], ids=["halo", "peer"])
+def test_slab_synth_matches_single_gpu_generator(peer, tmp_path):
     """dist.slab_synth (configs C4 / C5 inputs, generated slab by slab) vs the
     single-GPU synth_case: template and velocity to rounding, the reference
     image (64-step transport, fp32 slab path vs f64) within 1e-5."""
     import torch.multiprocessing as mp
 
-    mp.start_processes(_synth_worker, args=(2, _free_port(), 64, str(tmp_path)), nprocs=2, start_method="spawn",
-                       join=True)
+    mp.start_processes(_synth_worker, args=(2, _free_port(), 64, str(tmp_path), peer), nprocs=2,
+                       start_method="spawn", join=True)
     for r in range(2):
         res = json.load(open(os.path.join(tmp_path, f"synth{r}.json")))
         assert res["m0"] < 1e-7 and res["v"] < 1e-15 and res["m1"] < 1e-5, res
