@@ -121,6 +121,14 @@ struct PeerPlanes {
     const CUtensorMap* maps[3] = {nullptr, nullptr, nullptr};  // per field: nranks maps, rank r's window
     const float* base[3][PEER_MAX] = {};                       // per field, per rank: window base
 };
+// kernel argument: the peer tables in peer-mode instantiations, nothing in
+// the single-GPU / ghost-plane ones (no registers, branches or parameter
+// space spent on the common path)
+template <bool PEER>
+struct PeerArg : PeerPlanes {};
+template <>
+struct PeerArg<false> {};
+
 // owner rank and its local plane of local plane index b (|b| < n0g)
 __device__ __forceinline__ void peer_plane(const Dims& g, const PeerPlanes& pp, int b, int& owner, int& local) {
     int G = pp.rank * g.n0 + b;
@@ -253,9 +261,33 @@ template <int J = TB_J, int K = TB_K>
 __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float* __restrict__ src, const Dims& g,
                                            int lo0, int lo1, int lo2, int S0, int S1, int S2, int axis, int tid,
                                            int nthreads = BX * BY) {
-    const size_t plane = (size_t)g.n1 * g.n2;
-    patch_axis_f<J, K>(box, [&](int b) { return src + src_plane(g, b) * plane; }, g, lo0, lo1, lo2, S0, S1, S2, axis,
-                       tid, nthreads);
+    const int lo = axis == 0 ? lo0 : (axis == 1 ? lo1 : lo2);
+    const int S = axis == 0 ? S0 : (axis == 1 ? S1 : S2);
+    const int n = g.axis_len(axis);
+    const int a_end = lo < 0 ? min(-lo, S) : 0;
+    const int b_beg = lo + S > n ? max(n - lo, 0) : S;
+    const int cnt = a_end + (S - b_beg);
+    if (cnt == 0) return;
+    const int E1 = axis == 0 ? S1 : S0;
+    const int E2 = axis == 2 ? S1 : S2;
+    const int total = cnt * E1 * E2;
+    for (int e = tid; e < total; e += nthreads) {
+        int r = e / E2;
+        const int in2 = e - r * E2;
+        const int q = r / E1;
+        const int in1 = r - q * E1;
+        const int x = q < a_end ? q : b_beg + (q - a_end);
+        int a, b, c;
+        if (axis == 0) {
+            a = x; b = in1; c = in2;
+        } else if (axis == 1) {
+            a = in1; b = x; c = in2;
+        } else {
+            a = in1; b = in2; c = x;
+        }
+        const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
+        cp_async_elem<4>(box + (a * J + b) * K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));
+    }
 }
 
 // whole-box cp.async staging with wrap (grids smaller than the TMA box)
@@ -444,9 +476,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
         : "memory");
 }
 
-template <int M, int NF, class Op>
+template <int M, int NF, class Op, bool PEER>
 __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
-    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma, const __grid_constant__ PeerPlanes pp) {
+    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma, const __grid_constant__ PeerArg<PEER> pp) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
     extern __shared__ __align__(16) unsigned char sdyn[];
@@ -504,7 +536,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         S2 = (pe.w >> 20) & 1023;
         if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
             for (int b = 0; b < NB; ++b) {
-                if (pp.nranks)
+                if constexpr (PEER)
                     tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
                 else
                     tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
@@ -567,7 +599,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     S2 = mx2 + Halo<M>::hi - lo2 + 1;
     if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
         for (int b = 0; b < NB; ++b) {
-            if (pp.nranks)
+            if constexpr (PEER)
                 tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
             else
                 tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
@@ -594,7 +626,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
             if (use_tma) {
                 mbar_wait_sleep(&bars[f % NB], (unsigned)((f / NB) & 1));
                 if (wrap) {  // planes already wrapped by tma_box
-                    if (pp.nranks) {
+                    if constexpr (PEER) {
                         auto of = [&](int b) { return peer_plane_ptr(g, pp, f, b); };
                         patch_axis_f<TB_J, TB_K>(box, of, g, lo0, lo1, lo2, S0, S1, S2, 1, tid, BX * BY);
                         patch_axis_f<TB_J, TB_K>(box, of, g, lo0, lo1, lo2, S0, S1, S2, 2, tid, BX * BY);
@@ -630,7 +662,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
                 __syncthreads();  // every thread is done reading this buffer
                 if (tid == 0) {
                     fence_proxy_async();
-                    if (pp.nranks)
+                    if constexpr (PEER)
                         tma_box_peer(box, pp, f + NB, g, lo0, lo1, lo2, S0, &bars[f % NB]);
                     else
                         tma_box(box, &maps.m[f + NB], g, lo0, lo1, lo2, S0, &bars[f % NB]);
@@ -645,11 +677,15 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         for (int f = 0; f < NF; ++f) {
             const float* src = op.field(f);
 #pragma unroll
-            for (int u = 0; u < SL_TI; ++u)
-                vals[u][f] = !ok[u]      ? 0.f
-                             : pp.nranks ? peer_interp<M>(g, pp, f, base0[u], base1[u], base2[u], fr0[u], fr1[u], fr2[u])
-                                         : global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u],
-                                                                          base2[u], fr0[u], fr1[u], fr2[u]);
+            for (int u = 0; u < SL_TI; ++u) {
+                if constexpr (PEER)
+                    vals[u][f] = ok[u] ? peer_interp<M>(g, pp, f, base0[u], base1[u], base2[u], fr0[u], fr1[u], fr2[u])
+                                       : 0.f;
+                else
+                    vals[u][f] = ok[u] ? global_interp<float, M, float>(gsrc, src, base0[u] + g.h0, base1[u],
+                                                                        base2[u], fr0[u], fr1[u], fr2[u])
+                                       : 0.f;
+            }
         }
     }
     if constexpr (HasTileSmem<Op>::value) {
@@ -706,12 +742,23 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
             memset(&maps.m[f], 0, sizeof(CUtensorMap));
     }
     constexpr size_t smem = SlfSmem<NF>::bytes;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        FRG_CUDA(cudaFuncSetAttribute(k_slf<M, NF, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
+    static bool attr_set[2] = {false, false};  // per instantiation
+    if (!attr_set[peer]) {
+        if (peer)
+            FRG_CUDA(cudaFuncSetAttribute(k_slf<M, NF, Op, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        else
+            FRG_CUDA(cudaFuncSetAttribute(k_slf<M, NF, Op, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr_set[peer] = true;
     }
-    k_slf<M, NF, Op><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, pp);
+    if (peer) {
+        PeerArg<true> pa;
+        static_cast<PeerPlanes&>(pa) = pp;
+        k_slf<M, NF, Op, true><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, pa);
+    } else {
+        k_slf<M, NF, Op, false><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, PeerArg<false>());
+    }
     FRG_CHECK_LAUNCH();
 }
 
