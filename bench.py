@@ -80,12 +80,18 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a few hundred ms to start sampling: wait for its
+            # first row so that the samples kept (from here on) cover the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
+        self.start = len(self.rows)
         return self
 
     def _read(self):
@@ -102,8 +108,10 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[self.start:] or self.rows[-1:]  # samples taken during the timed region
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.rows = rows
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -198,12 +206,19 @@ def run_b200(a):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0 = st.matvecs
+    # the dominant kernel (IncFirstOp: 3-field gather of v~ at the feet + all
+    # Heun sources, 22% of the step) timed live: CUDA events on its own stream
+    # bracket each of its launches inside the timed matvecs (frg_probe_*)
+    L.check(L.lib().frg_probe_arm(1), "probe_arm")
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(a.steps):
             st.hessian_matvec(vt, out=out)
         e1.record(stream)
         torch.cuda.synchronize()
+    L.check(L.lib().frg_probe_arm(0), "probe_arm")
+    probe_ms, probe_n = ctypes.c_double(), ctypes.c_int64()
+    L.check(L.lib().frg_probe_read(ctypes.byref(probe_ms), ctypes.byref(probe_n)), "probe_read")
     barrier()
     torch.cuda.synchronize()
     assert st.matvecs - c0 == a.steps
@@ -259,6 +274,12 @@ def run_b200(a):
     peak, peak_src = peaks()
     achieved = alg_bytes / t_gather / 1e9
     traffic = profile_traffic().get("k_gather_cubic_f32_bytes_per_launch")
+    # IncFirstOp algorithmic bytes per voxel (fp32, d = 3): disp 12 + v~ 12 (gather
+    # source and the x-side Heun term read the same array: counted once) +
+    # grad m_j(y) n_t*12 + grad m_{j+1}(x) n_t*12, writes m~_1 4 + S_1..S_{n_t-1} 4 (n_t - 1)
+    nt_ = 4
+    inc_bytes = N * (12 + 12 + 12 * nt_ + 12 * nt_ + 4 + 4 * (nt_ - 1))
+    t_inc = probe_ms.value / 1e3 / max(probe_n.value, 1)
 
     # whole-matvec roofline with the canonical field-pass count (174 F)
     canon = 174 * 4 * N
@@ -398,9 +419,21 @@ def run_b200(a):
             "data": "synthetic (synth_case rotation, generated on device)",
             "config": dict(config(n, a.precision), parallelism="single GPU"),
             "e2e": e2e, "gpu_launches": gpu_launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> (one TMA-staged SL gather step with its tile plan, frg_gather_planned)",
-                         "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather, "peak_source": peak_src},
+            "roofline": {"bound": "hbm", "achieved": inc_bytes / t_inc / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": inc_bytes / t_inc / 1e9 / peak,
+                         "traffic": profile_traffic().get("k_incfirst_bytes_per_launch"),
+                         "kernel": "k_slf<CUBIC,3,IncFirstOp<float,3>>: the step's dominant kernel (fused 3-field "
+                                   "gather of v~ at the feet + every Heun source S_j), timed live inside the timed "
+                                   "matvecs (CUDA events on its stream, frg_probe_*)",
+                         "algorithmic_bytes_per_launch": inc_bytes, "bytes_per_voxel": inc_bytes // N,
+                         "launch_s": t_inc, "launches_timed": probe_n.value, "peak_source": peak_src},
+            "gather_roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                                "frac": achieved / peak, "traffic": traffic,
+                                "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> (one TMA-staged SL gather step with its "
+                                          "tile plan, frg_gather_planned; the 7 single-field SL steps of the matvec "
+                                          "run this engine; shared-memory bound, DESIGN.md §5)",
+                                "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather,
+                                "peak_source": peak_src},
             "matvec_roofline": matvec_roofline,
             "time_to_solution": tts,
             "clocks": clk.summary(),

@@ -173,6 +173,12 @@ int frg_kkt_destroy(frg_kkt* k);
 /* Destroyed contexts park their device buffers for the next context (capped
    at FRG_POOL_CAP_MB, default 1/4 of device memory); this frees them all. */
 int frg_release_pool(void);
+/* Measurement probe (bench.py): while armed, CUDA events on the launching
+ * stream bracket every launch of the GN matvec's incremental-state first step
+ * (the fused 3-field gather + Heun sources, its dominant kernel); read returns
+ * the summed duration and the launch count and disarms nothing. */
+int frg_probe_arm(int32_t on);
+int frg_probe_read(double* total_ms, int64_t* count);
 /* Peer windows of the slab path without ghost planes (dist.py peer mode; no
  * reference counterpart — the north star's off-rank departure-point exchange,
  * PAPER.md:545).  A window holds one rank's owned planes (n_loc) of a gathered

@@ -76,6 +76,8 @@ PROTOTYPES = {
     "frg_prolong": [_N3, _I, _P, _P, _P],
     "frg_dot": [_I, _P, _P, _L, _DP, _P],
     "frg_release_pool": [],
+    "frg_probe_arm": [_I],
+    "frg_probe_read": [_DP, ctypes.POINTER(_L)],
     "frg_peer_alloc": [_L, ctypes.POINTER(_P), _P],
     "frg_peer_free": [_P],
     "frg_peer_open": [_P, ctypes.POINTER(_P)],

@@ -389,6 +389,17 @@ int frg_peer_unregister(const void* local) {
     return guard([&] { peer_unregister((const float*)local); });
 }
 
+int frg_probe_arm(int32_t on) {
+    return guard([&] { probe_arm(on != 0); });
+}
+int frg_probe_read(double* total_ms, int64_t* count) {
+    return guard([&] {
+        long long c = 0;
+        probe_read(total_ms, &c);
+        *count = c;
+    });
+}
+
 int frg_release_pool(void) {
     return guard([&] { kkt_release_pool(); });
 }

@@ -162,4 +162,8 @@ void* ipc_alloc(size_t bytes, void* handle);
 void* ipc_open(const void* handle);
 void ipc_close(void* p);
 
+// launch probe of the GN matvec's IncFirstOp kernel (transport_inc.cu)
+void probe_arm(bool on);
+void probe_read(double* total_ms, long long* count);
+
 }  // namespace frg

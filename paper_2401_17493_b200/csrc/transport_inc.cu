@@ -3,8 +3,60 @@
 #include "sl_half.cuh"
 
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 namespace frg {
+
+// Launch probe for bench.py: while armed, CUDA events bracket every IncFirstOp
+// launch (the GN matvec's dominant kernel) on its own stream; frg_probe_read
+// sums their durations.  Off (two branches per matvec) unless armed.
+namespace {
+struct Probe {
+    bool armed = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+};
+Probe& probe() {
+    static Probe p;
+    return p;
+}
+}  // namespace
+
+void probe_arm(bool on) { probe().armed = on; }
+
+void probe_read(double* total_ms, long long* count) {
+    Probe& p = probe();
+    double t = 0.0;
+    for (auto& e : p.ev) {
+        FRG_CUDA(cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        FRG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+        t += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    *total_ms = t;
+    *count = (long long)p.ev.size();
+    p.ev.clear();
+}
+
+template <class F>
+static void probed(cudaStream_t st, F&& launch) {
+    Probe& p = probe();
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (p.armed) cudaStreamIsCapturing(st, &cs);
+    if (!p.armed || cs != cudaStreamCaptureStatusNone) {
+        launch();
+        return;
+    }
+    cudaEvent_t a, b;
+    FRG_CUDA(cudaEventCreate(&a));
+    FRG_CUDA(cudaEventCreate(&b));
+    FRG_CUDA(cudaEventRecord(a, st));
+    launch();
+    FRG_CUDA(cudaEventRecord(b, st));
+    p.ev.emplace_back(a, b);
+}
 
 // ---------------------------------------------------------------------------
 // incremental state (transport.py:147-176)
@@ -202,7 +254,7 @@ static void inc_state_d(const Dims& g, int method, int n_t, const T* disp, const
         op.S = S;
         op.fsign = fsign;
         op.hh = T(0.5) * ht;
-        launch_sl<T, D>(g, method, op, st);
+        probed(st, [&] { launch_sl<T, D>(g, method, op, st); });
     }
     for (int j = 1; j < n_t; ++j) {
         bool last = (j == n_t - 1);
