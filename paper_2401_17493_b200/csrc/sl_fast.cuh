@@ -96,6 +96,18 @@ __device__ __forceinline__ void tma_load_2d(float* dst, const CUtensorMap* map, 
         "l"((unsigned long long)map), "r"(col), "r"(row), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"((unsigned long long)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// host: 3D tiled map over `planes` stacked fp32 (n1, n2) planes, box 4 planes x BY rows x BX columns
+// (the per-voxel streams of one SL tile)
+void encode_tile_stream_map(CUtensorMap* map, const float* ptr, int n1, int n2, long long planes);
+
 // issue the S0 plane loads of one field box (one thread)
 template <int PLANE = TB_PLANE>
 __device__ __forceinline__ void tma_box(float* box, const CUtensorMap* map, const Dims& g, int lo0, int lo1, int lo2,
@@ -478,7 +490,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
 
 template <int M, int NF, class Op, bool PEER>
 __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
-    k_slf(Dims g, Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma, const __grid_constant__ PeerArg<PEER> pp) {
+    k_slf(Dims g, const __grid_constant__ Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma,
+          const __grid_constant__ PeerArg<PEER> pp) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
     static_assert(SL_TI % 2 == 0, "k_slf pairs the voxels of a thread");
     extern __shared__ __align__(16) unsigned char sdyn[];
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     // that the taps compile to LDS, not generic LD
     float* sbox = reinterpret_cast<float*>(sdyn + ((1024u - (smem_u32(sdyn) & 1023u)) & 1023u));
     constexpr int NB = SlfSmem<NF>::NB;
-    __shared__ __align__(8) uint64_t bars[NB];
+    __shared__ __align__(8) uint64_t bars[NB + 1];  // + the epilogue's (done_tile_smem TMA rounds)
     __shared__ int bb[6];  // min0, min1, min2, -max0, -max1, -max2 of the stencil bases
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
     const int k = blockIdx.x * BX + tx;
@@ -494,7 +507,7 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     const int i_base = blockIdx.z * SL_TI;
     const bool in_kj = (k < g.n2) && (j < g.n1);
     if (tid == 0) {
-        for (int b = 0; b < NB; ++b) mbar_init(&bars[b], 1);
+        for (int b = 0; b <= NB; ++b) mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (tid < 6) bb[tid] = INT_MAX;
@@ -692,7 +705,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         if (fits && 12 * SL_TI * BX * BY <= TB_VOL) {
             __syncthreads();  // the box is free once every thread is done with the last gather
             op.template done_tile_smem<SL_TI>((i_base * g.n1 + j) * g.n2 + k, g.n1 * g.n2, ok, vals, sbox, tid,
-                                              BX * BY);
+                                              BX * BY, &bars[NB], use_tma,
+                                              make_int3(blockIdx.x * BX, blockIdx.y * BY, i_base));
             return;
         }
     }

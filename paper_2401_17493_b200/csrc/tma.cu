@@ -38,6 +38,18 @@ void encode_field_map(CUtensorMap* map, const float* ptr, const Dims& g, int box
     if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+void encode_tile_stream_map(CUtensorMap* map, const float* ptr, int n1, int n2, long long planes) {
+    FRG_REQUIRE(((uintptr_t)ptr & 15) == 0 && n2 % 4 == 0, "tile-stream TMA: 16-byte aligned rows");
+    const cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)n2 * 4, (cuuint64_t)n1 * n2 * 4};
+    const cuuint32_t box[3] = {BX, BY, SL_TI};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ptr, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(E_CUDA, "cuTensorMapEncodeTiled (tile stream) failed (" + std::to_string((int)r) + ")");
+}
+
 void encode_field_map_half(CUtensorMap* map, const __half* ptr, const Dims& g) {
     FRG_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA field must be 16-byte aligned");
     FRG_REQUIRE(g.n2 % 8 == 0, "fp16 TMA rows must be multiples of 16 bytes");
