@@ -102,6 +102,9 @@ __device__ __forceinline__ int wrap1(int i, int n) {
 }
 
 constexpr int ROW_WARPS = 8;
+#ifndef FRG_FIR_ROW_BLOCKS_PER_SM
+#define FRG_FIR_ROW_BLOCKS_PER_SM 16
+#endif
 // shared index of row element e: one pad word per Q elements, so the lanes'
 // windows (lane * Q + j) fall on 32 distinct banks (Q + 1 odd)
 template <int Q>
@@ -219,7 +222,7 @@ void fir_pass(const Dims& g, int axis, const T* in, T* out, cudaStream_t st) {
     if (axis == 2) {
         const long long nrows = (long long)g.n0 * g.n1;
         const long long work = nrows * ((g.n2 + ROW_SEG - 1) / ROW_SEG);
-        const int blocks = (int)std::min<long long>((work + ROW_WARPS - 1) / ROW_WARPS, 148LL * 16);
+        const int blocks = (int)std::min<long long>((work + ROW_WARPS - 1) / ROW_WARPS, 148LL * FRG_FIR_ROW_BLOCKS_PER_SM);
         k_fir_row<T><<<blocks, 32 * ROW_WARPS, 0, st>>>(in, out, g.n2, nrows, taps);
     } else {
         const long long lstride = axis == 1 ? g.n2 : (long long)g.n1 * g.n2;
