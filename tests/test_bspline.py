@@ -1,9 +1,13 @@
 """Cubic B-spline interpolation (north-star extension, method "bspline").
 
-The reference package has no B-spline path, so parity is
-UNPINNED against the reference; these tests pin the CPU restatement
-(oracle.sample_bspline) by its defining properties and the CUDA path against
-the restatement:
+The reference package has no B-spline path, so parity cannot
+be pinned to the reference; it is pinned to an independent published
+implementation instead — scipy.ndimage.map_coordinates(order=3,
+mode="grid-wrap", prefilter=True) (scipy 1.x, the periodic cubic B-spline
+interpolant with the same prefilter) — and by the interpolant's defining
+properties:
+* oracle.sample_bspline == scipy and CUDA sample_nd("bspline") == scipy at
+  random points (f64 1e-12);
 * interpolation condition — the interpolant reproduces the samples at every
   node (prefilter exactness);
 * 4th-order accuracy on a smooth periodic function;
@@ -14,6 +18,17 @@ import numpy as np
 import pytest
 
 from oracle import flowreg_oracle as O
+
+
+def test_oracle_bspline_matches_scipy():
+    ndimage = pytest.importorskip("scipy.ndimage")
+    rng = np.random.default_rng(7)
+    for shape in ((12, 10, 16), (20, 24)):
+        u = rng.standard_normal(shape)
+        qs = [rng.uniform(-5, n + 5, 800) for n in shape]
+        ref = ndimage.map_coordinates(u, np.array(qs), order=3, mode="grid-wrap", prefilter=True)
+        got = O.sample_bspline(u, qs)
+        assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-13
 
 
 def test_oracle_bspline_interpolates_nodes():
@@ -42,6 +57,20 @@ def _gpu():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     return torch
+
+
+@pytest.mark.gpu
+def test_sample_nd_bspline_matches_scipy():
+    _gpu()
+    ndimage = pytest.importorskip("scipy.ndimage")
+    from paper_2401_17493_b200._kernels import sample_nd
+
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((16, 24, 32))
+    qs = [rng.uniform(-5, n + 5, 4000) for n in u.shape]
+    ref = ndimage.map_coordinates(u, np.array(qs), order=3, mode="grid-wrap", prefilter=True)
+    got = sample_nd(u, qs, "bspline")
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
 
 
 @pytest.mark.gpu
