@@ -491,12 +491,18 @@ def run_slab(a, F, L, world, rank, local, backend):
     b0 = comm.bytes_sent
     c0 = st.matvecs
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.check(L.lib().frg_probe_arm(1), "probe_arm")  # the dominant kernel (slab IncFirstOp), live
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(a.steps):
             st.hessian_matvec(vt, out=out)
         e1.record(stream)
         torch.cuda.synchronize()
+    L.check(L.lib().frg_probe_arm(0), "probe_arm")
+    probe_ms, probe_n = ctypes.c_double(), ctypes.c_int64()
+    L.check(L.lib().frg_probe_read(ctypes.byref(probe_ms), ctypes.byref(probe_n)), "probe_read")
+    t_inc = max_over_ranks(probe_ms.value / 1e3 / max(probe_n.value, 1))
+    inc_bytes = n0l * n * n * (12 + 12 + 48 + 48 + 4 + 12)  # IncFirstOp, 136 B/voxel (see run_b200)
     barrier()
     torch.cuda.synchronize()
     assert st.matvecs - c0 == a.steps
@@ -592,11 +598,17 @@ def run_slab(a, F, L, world, rank, local, backend):
                     "steps": e2e_steps, "path": "pinned host v~ slab per rank -> DistKktState.hessian_matvec -> "
                                                 "pinned host, serial per step"},
             "gpu_launches": launches * a.steps,
-            "roofline": {"bound": "hbm", "achieved": alg_bytes / t_gather / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": alg_bytes / t_gather / 1e9 / peak, "traffic": None,
-                         "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> on this rank's slab (frg_slab_gather, tile plan, "
-                                   "ghost planes)", "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_gather,
-                         "peak_source": peak_src},
+            "roofline": {"bound": "hbm", "achieved": inc_bytes / t_inc / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": inc_bytes / t_inc / 1e9 / peak, "traffic": None,
+                         "kernel": "k_slf<CUBIC,3,IncFirstOp<float,3>> on this rank's slab (the matvec's dominant "
+                                   "kernel, timed live inside the timed matvecs, max over ranks)",
+                         "algorithmic_bytes_per_launch": inc_bytes, "launch_s": t_inc,
+                         "launches_timed": probe_n.value, "peak_source": peak_src},
+            "gather_roofline": {"bound": "hbm", "achieved": alg_bytes / t_gather / 1e9, "peak": peak,
+                                "unit": "GB/s", "frac": alg_bytes / t_gather / 1e9 / peak, "traffic": None,
+                                "kernel": "k_slf<CUBIC,1,GatherOp<float,1>> on this rank's slab (frg_slab_gather, "
+                                          "tile plan)", "algorithmic_bytes_per_launch": alg_bytes,
+                                "launch_s": t_gather, "peak_source": peak_src},
             "matvec_roofline": {"canonical_bytes_per_rank": canon, "achieved_gbs": canon / (t / a.steps) / 1e9,
                                 "peak_gbs": peak, "frac": canon / (t / a.steps) / 1e9 / peak,
                                 "note": "SURVEY.md §8d canonical 174 fp32 field passes per matvec, per rank"},

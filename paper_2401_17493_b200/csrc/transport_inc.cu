@@ -354,7 +354,7 @@ void inc_first(const Dims& g, int method, int n_t, const float* disp, const floa
     op.fsign = 0.f;
     op.hh = 0.5f * (float)(1.0 / n_t);
     set_tile_streams(op, g, n_t);
-    launch_sl<float, 3>(g, method, op, st);
+    probed(st, [&] { launch_sl<float, 3>(g, method, op, st); });
 }
 
 void inc_step(const Dims& g, int method, const float* disp, const float* m_src, const float* Sj, float* m_next,
