@@ -488,6 +488,22 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
         : "memory");
 }
 
+// Programmatic dependent launch (PDL): every SL step lets the next launch
+// start as soon as all of its CTAs are resident, and waits for its
+// predecessor's results only where it reads them — the plan / displacement
+// loads and the stencil bases of step j+1 overlap the tail of step j (the
+// displacement maps and plans of a solve are built long before its steps).
+// Ops whose displacement is produced by the preceding SL launch (ComposeOp,
+// DepartureOp's velocity) declare kLateDisp and wait before any load.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+template <class Op, class = void>
+struct LateDisp : std::false_type {};
+template <class Op>
+struct LateDisp<Op, std::void_t<decltype(Op::kLateDisp)>> : std::bool_constant<Op::kLateDisp> {};
+
 template <int M, int NF, class Op, bool PEER>
 __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
     k_slf(Dims g, const __grid_constant__ Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma,
@@ -512,6 +528,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     }
     if (tid < 6) bb[tid] = INT_MAX;
     __syncthreads();  // barrier + bb initialised before anyone uses them (nothing is in flight yet)
+    griddep_launch_dependents();
+    if constexpr (LateDisp<Op>::value) griddep_wait();
 
     const int4* plan = nullptr;
     if constexpr (HasDs<Op>::value) plan = op.ds.plan;
@@ -529,6 +547,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
         if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, dsp[u][0], dsp[u][1], dsp[u][2]);
     }
+    // the gathered sources and epilogue inputs may be the predecessor's outputs
+    if constexpr (!LateDisp<Op>::value) griddep_wait();
     using PreT = typename PreOf<Op>::type;
     PreT pre[SL_TI];
     if constexpr (HasPre<Op>::value) {
@@ -766,12 +786,27 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
                                           (int)smem));
         attr_set[peer] = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = sl_grid(g);
+    cfg.blockDim = vox_block();
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    // not inside CUDA-graph capture (the small-grid matvec graph measured
+    // 151 -> 160 us at 64^3 with programmatic edges; eager launches gain)
+    static const bool pdl = getenv("FRG_NO_PDL") == nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (pdl) FRG_CUDA(cudaStreamIsCapturing(st, &cs));
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && cs == cudaStreamCaptureStatusNone) ? 1 : 0;
     if (peer) {
         PeerArg<true> pa;
         static_cast<PeerPlanes&>(pa) = pp;
-        k_slf<M, NF, Op, true><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, pa);
+        FRG_CUDA(cudaLaunchKernelEx(&cfg, k_slf<M, NF, Op, true>, g, op, maps, use_tma, pa));
     } else {
-        k_slf<M, NF, Op, false><<<sl_grid(g), vox_block(), smem, st>>>(g, op, maps, use_tma, PeerArg<false>());
+        FRG_CUDA(cudaLaunchKernelEx(&cfg, k_slf<M, NF, Op, false>, g, op, maps, use_tma, PeerArg<false>()));
     }
     FRG_CHECK_LAUNCH();
 }

@@ -77,6 +77,7 @@ void sample_q(const void* vals, int dtype, const Dims& g, const double* q0, cons
 template <typename T, typename VI, int D>
 struct DepartureOp {
     using V = VI;
+    static constexpr bool kLateDisp = true;  // displacement from the preceding launch (PDL, sl_fast.cuh)
     const VI* v[3];      // per component: gathered source (slab: with ghost planes)
     const VI* vl[3];     // per component: v at the output voxels
     T sc[3];             // per component: h_t / h_axis

@@ -137,6 +137,7 @@ void deformation_tensor(const Dims& g, int tdtype, int method, int n_t, const vo
 template <typename T, int D>
 struct ComposeOp {
     using V = T;
+    static constexpr bool kLateDisp = true;  // displacement from the preceding launch (PDL, sl_fast.cuh)
     DispSrc<T> cur;
     const T* step[D];
     const T* Din[D];
