@@ -21,6 +21,8 @@
 //    (rows of 32 contiguous columns, coalesced, every load in flight at
 //    once), each thread produces R runs of Q consecutive outputs of one
 //    column from register windows (a warp reads one smem row: 32 banks).
+#include <cstdlib>
+
 #include "ops.h"
 #include "spectral.h"
 
@@ -118,6 +120,10 @@ __global__ void __launch_bounds__(32 * ROW_WARPS) k_fir_row(const T* __restrict_
     constexpr int SMN = ROW_SEG + 2 * K + (ROW_SEG + 2 * K) / Q + 1;
     __shared__ T sm[ROW_WARPS][SMN];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // PDL: let the next pass / SL step start its prologue, read only after the
+    // predecessor (the producing step or the previous pass) has completed
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const int nseg = (n2 + ROW_SEG - 1) / ROW_SEG;
     const int nwork = (int)(nrows * nseg);  // < 2^31 for every grid the engine takes (<= 1024^3)
     for (int item = blockIdx.x * ROW_WARPS + w; item < nwork; item += gridDim.x * ROW_WARPS) {
@@ -167,6 +173,8 @@ __global__ void __launch_bounds__(256) k_fir_col(const T* __restrict__ in, T* __
     constexpr int K = FirK<T>::K, Q = FirK<T>::Q, W = Q + 2 * K, COL_SEG = 8 * Q * COL_R, ROWS = COL_SEG + 2 * K;
     __shared__ T sm[ROWS][32];
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const int c = blockIdx.x * 32 + tx;
     const int l0 = blockIdx.y * COL_SEG;
     const long long base = (long long)blockIdx.z * ostride;
@@ -198,6 +206,25 @@ __global__ void __launch_bounds__(256) k_fir_col(const T* __restrict__ in, T* __
     }
 }
 
+// programmatic dependent launch (as the SL steps, sl_fast.cuh), off inside graph capture
+template <typename K, typename... Args>
+void pdl_launch(K kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool pdl = getenv("FRG_NO_PDL") == nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (pdl) FRG_CUDA(cudaStreamIsCapturing(st, &cs));
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && cs == cudaStreamCaptureStatusNone) ? 1 : 0;
+    FRG_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 struct FirScratch {
     void* p = nullptr;
     size_t cap = 0;
@@ -223,13 +250,13 @@ void fir_pass(const Dims& g, int axis, const T* in, T* out, cudaStream_t st) {
         const long long nrows = (long long)g.n0 * g.n1;
         const long long work = nrows * ((g.n2 + ROW_SEG - 1) / ROW_SEG);
         const int blocks = (int)std::min<long long>((work + ROW_WARPS - 1) / ROW_WARPS, 148LL * FRG_FIR_ROW_BLOCKS_PER_SM);
-        k_fir_row<T><<<blocks, 32 * ROW_WARPS, 0, st>>>(in, out, g.n2, nrows, taps);
+        pdl_launch(k_fir_row<T>, dim3(blocks), dim3(32 * ROW_WARPS), st, in, out, g.n2, nrows, taps);
     } else {
         const long long lstride = axis == 1 ? g.n2 : (long long)g.n1 * g.n2;
         const long long ostride = axis == 1 ? (long long)g.n1 * g.n2 : g.n2;
         const int nouter = axis == 1 ? g.n0 : g.n1;
         dim3 grid((g.n2 + 31) / 32, (n + COL_SEG - 1) / COL_SEG, nouter);
-        k_fir_col<T><<<grid, dim3(32, 8), 0, st>>>(in, out, n, lstride, ostride, g.n2, taps);
+        pdl_launch(k_fir_col<T>, grid, dim3(32, 8), st, in, out, n, lstride, ostride, g.n2, taps);
     }
     FRG_CHECK_LAUNCH();
 }
