@@ -397,13 +397,17 @@ class DistKktState:
     of per-rank slab kernels and exchanges; all ranks call them in lockstep."""
 
     def __init__(self, m0: torch.Tensor, m1: torch.Tensor, reg: RegConfig, comm: SlabComm, n_glob, n_t: int = 4,
-                 method: str = "cubic", v_init: torch.Tensor | None = None, peer: bool | None = None):
+                 method: str = "cubic", v_init: torch.Tensor | None = None, peer: bool | None = None,
+                 distance: str = "ssd"):
         """``peer=True`` (default: env FRG_SLAB_PEER=1): SL gathers read off-rank
         stencil planes from the owners' peer windows (PeerWindows) instead of
         exchanging ghost slabs of width ceil(max |disp_0|) + 2; FD8 keeps its
         4 ghost planes."""
         if method not in ("linear", "cubic", "bspline"):
             raise ValueError("slab transport supports linear / cubic / bspline interpolation")
+        if distance not in ("ssd", "ncc"):
+            raise ValueError(f"unknown distance measure {distance!r}")
+        self.distance = distance
         self.comm = comm
         self.grid = SlabGrid(tuple(int(v) for v in n_glob), comm.rank, comm.size, n_t=n_t)
         self.peer = (os.environ.get("FRG_SLAB_PEER") == "1") if peer is None else bool(peer)
@@ -429,7 +433,7 @@ class DistKktState:
         self.matvecs = 0
         self.pde_solves = 0
         self.precond_fallbacks = 0
-        self._init_mismatch = self._ssd(self.m0)
+        self._init_mismatch = self._dist_value(self.m0)
         v0 = torch.zeros((3, *g.n), dtype=torch.float64, device="cuda") if v_init is None else v_init
         self.refresh(v0)
 
@@ -512,6 +516,45 @@ class DistKktState:
     def _ssd(self, md: torch.Tensor) -> float:
         r = md - self.m1
         return 0.5 * self.dot(r, r) * self.grid.cell_volume
+
+    # -- distance measures (distance.py:34-91), global moments all-reduced ----
+    def _ncc_moments(self, md: torch.Tensor):
+        cv = self.grid.cell_volume
+        a, b, c = self.dot(self.m1, md) * cv, self.dot(md, md) * cv, self.dot(self.m1, self.m1) * cv
+        if b <= 0.0 or c <= 0.0:
+            from .distance import ZeroNormError
+
+            raise ZeroNormError("normalized cross correlation needs nonzero images")
+        return a, b, c
+
+    def _dist_value(self, md: torch.Tensor) -> float:
+        if self.distance == "ssd":
+            return self._ssd(md)
+        a, b, c = self._ncc_moments(md)
+        return 1.0 - (a * a) / (b * c)
+
+    def _adjoint_final(self, md: torch.Tensor, out: torch.Tensor) -> None:
+        """lambda(1) = minus the mismatch gradient in md (distance.py:58-68)."""
+        if self.distance == "ssd":
+            torch.sub(self.m1, md, out=out)
+            return
+        a, b, c = self._ncc_moments(md)
+        f = -2.0 * a / (b * c)
+        torch.mul(md, f * a / b, out=out)
+        out.add_(self.m1, alpha=-f)
+
+    def _incremental_final(self, mt: torch.Tensor, out: torch.Tensor) -> None:
+        """lambda~(1), the GN final condition of the incremental dual
+        (distance.py:71-91; SSD is fused into the last incremental step)."""
+        md = self.mseries[-1]
+        a, b, c = self._ncc_moments(md)
+        cv = self.grid.cell_volume
+        mm, rm = self.dot(md, mt) * cv, self.dot(self.m1, mt) * cv
+        q1 = 2.0 * a * mm / b ** 2 - rm / b
+        q2 = 4.0 * a * a * mm / b ** 3 - 2.0 * a * rm / b ** 2
+        q3 = a * a / b ** 2
+        torch.mul(self.m1, -2.0 * q1 / c, out=out)
+        out.add_(md, alpha=2.0 * q2 / c).add_(mt, alpha=-2.0 * q3 / c)
 
     def _gather(self, disp, W, srcs, outs):
         ins = (ctypes.c_void_p * len(srcs))(*[s.data_ptr() for s in srcs])
@@ -596,10 +639,11 @@ class DistKktState:
                                                     _c(self.disp_b), _c(self._src(divv, self.Wb)), _c(divv),
                                                     _c(self.cmul), L.stream()), "slab_adjoint_multiplier")
         self.lam = torch.empty((g.n_t + 1, *g.n), dtype=torch.float32, device="cuda")
-        torch.sub(self.m1, self.mseries[-1], out=self.lam[g.n_t])  # -(m(1) - m1), SSD
+        self._adjoint_final(self.mseries[-1], self.lam[g.n_t])
         self._adjoint(self.lam)
         self.pde_solves += 2
         self._dist = None
+        self._h0_grad = None
 
     def _adjoint(self, series):
         g = self.grid
@@ -652,14 +696,18 @@ class DistKktState:
             return series[j]
 
         lt = torch.empty((g.n_t + 1, n0l + 2 * Wb, *g.n[1:]), dtype=torch.float32, device="cuda")
+        ssd = self.distance == "ssd"
         for j in range(1, g.n_t):
             src = source(mt, j, Wf)
-            last = j == g.n_t - 1  # the last step writes lam~(1) = -m~(1) (SSD) straight into the adjoint series
+            # SSD: the last step writes lam~(1) = -m~(1) straight into the adjoint series
+            last = ssd and j == g.n_t - 1
             L.check(L.lib().frg_slab_inc_step(self.n_loc, g.n_glob[0], Wf, self._m, _c(self.disp_f), _c(src),
                                               _c(S[j - 1]), None if last else _c(own_f(j + 1)),
                                               _c(lt[g.n_t, Wb:Wb + n0l]) if last else None, -1.0, L.stream()),
                     "slab_inc_step")
-        if g.n_t == 1:
+        if not ssd:
+            self._incremental_final(own_f(g.n_t), lt[g.n_t, Wb:Wb + n0l])
+        elif g.n_t == 1:
             torch.neg(own_f(1), out=lt[1, Wb:Wb + n0l])
         for j in range(g.n_t, 0, -1):
             src = source(lt, j, Wb)
@@ -677,13 +725,203 @@ class DistKktState:
 
     def apply_precond(self, r, kind: PrecondKind | None = None, outer_tol: float = 0.0,
                       out: torch.Tensor | None = None) -> _Vec:
-        """kkt.py:308-311 ('reg': the spectral inverse of alpha L)."""
-        if kind is not None and kind.kind != "reg":
-            raise ValueError("the slab path implements the 'reg' preconditioner")
+        """kkt.py:308-324: 'reg' (the spectral inverse of alpha L) and 'h0'
+        (nested PCG on the zero-velocity Hessian surrogate, 'reg'
+        preconditioned; breakdown falls back to 'reg' and counts)."""
         rd = (r.data if hasattr(r, "data") else r).to(self._spec_dt).contiguous()
+        if kind is not None and kind.kind == "2level":
+            res = self._two_level(rd, kind, outer_tol)
+            if res is not None:
+                if out is None:
+                    return _Vec(self.grid, res)
+                out.copy_(res)
+                return _Vec(self.grid, out)
+            self.precond_fallbacks += 1
+        elif kind is not None and kind.kind == "h0":
+            sol, broke = self._inner_pcg(self._apply_h0, rd, kind.inner_tol_factor * outer_tol,
+                                         kind.inner_max_iterations)
+            if not broke:
+                if out is None:
+                    return _Vec(self.grid, sol)
+                out.copy_(sol)
+                return _Vec(self.grid, out)
+            self.precond_fallbacks += 1
         out = torch.empty_like(rd) if out is None else out
         self.fft.apply(rd, "reg_inv", self._reg, out=out)
         return _Vec(self.grid, out)
+
+    # -- two-level preconditioner (kkt.py:291-306,325-341) -------------------
+    # The coarse problem (n/2 per axis, 1/8 of the unknowns) is solved
+    # redundantly on every rank: restrict = the slab forward spectrum's bins
+    # |k_i| < n_i/4 (diffops.py:304-327), placed by their owners into a zeroed
+    # full coarse half-spectrum and summed over ranks (one all-reduce); the
+    # coarse PCG runs with single-GPU kernels and rank-local inner products
+    # (identical on every rank); prolong = the coarse spectrum written back
+    # into each rank's fine spectrum rows + a slab inverse (diffops.py:330-343).
+    def _coarse_maps(self):
+        if getattr(self, "_cmaps", None) is None:
+            n0, n1, n2 = self.grid.n_glob
+
+            def kept(n):  # diffops.py:304-310: fine bins kept, their coarse bins
+                nc = n // 2
+                f = list(range(0, nc // 2)) + list(range(n - nc // 2 + 1, n))
+                c = list(range(0, nc // 2)) + list(range(nc - nc // 2 + 1, nc))
+                return f, c
+
+            f0, c0 = kept(n0)
+            f1, c1 = kept(n1)
+            lo, hi = self.fft.i1_off, self.fft.i1_off + self.fft.n1l
+            mine = [(a, b) for a, b in zip(f1, c1) if lo <= a < hi]
+            dev = lambda v: torch.tensor(v, dtype=torch.long, device="cuda")  # noqa: E731
+            self._cmaps = {"f0": dev(f0), "c0": dev(c0), "f1": dev([a - lo for a, _ in mine]),
+                           "c1": dev([b for _, b in mine]), "k2": n2 // 4, "nc": (n0 // 2, n1 // 2, n2 // 2)}
+        return self._cmaps
+
+    def _restrict(self, x: torch.Tensor) -> torch.Tensor:
+        """(C, n0_loc, n1, n2) slab -> (C, n0/2, n1/2, n2/2) full coarse field on every rank."""
+        cm = self._coarse_maps()
+        nc0, nc1, nc2 = cm["nc"]
+        C = x.shape[0]
+        spec = self.fft.forward(x.to(torch.float64).contiguous())
+        ch = torch.zeros((C, nc0, nc1, nc2 // 2 + 1), dtype=torch.complex128, device="cuda")
+        if cm["f1"].numel():
+            blk = spec.index_select(1, cm["f0"]).index_select(2, cm["f1"])[..., :cm["k2"]]
+            tmp = torch.zeros((C, nc0, cm["f1"].numel(), cm["k2"]), dtype=torch.complex128, device="cuda")
+            tmp.index_copy_(1, cm["c0"], blk)
+            ch[:, :, :, :cm["k2"]].index_copy_(2, cm["c1"], tmp)
+        if self.comm.size > 1:
+            rv = torch.view_as_real(ch)
+            if self.comm.staged:
+                h = rv.cpu()
+                tdist.all_reduce(h, group=self.comm.group)
+                rv.copy_(h)
+            else:
+                tdist.all_reduce(rv, group=self.comm.group)
+        nf, nc = float(np.prod(self.grid.n_glob)), float(nc0 * nc1 * nc2)
+        return torch.fft.irfftn(ch * (nc / nf), s=(nc0, nc1, nc2), dim=(1, 2, 3))
+
+    def _prolong(self, xc: torch.Tensor) -> torch.Tensor:
+        """(C, n0/2, n1/2, n2/2) full coarse field -> (C, n0_loc, n1, n2) slab (zero padding)."""
+        cm = self._coarse_maps()
+        nc0, nc1, nc2 = cm["nc"]
+        C = xc.shape[0]
+        ch = torch.fft.rfftn(xc, dim=(1, 2, 3))
+        spec = torch.zeros((C, self.grid.n_glob[0], self.fft.n1l, self.fft.nh), dtype=torch.complex128,
+                           device="cuda")
+        if cm["f1"].numel():
+            blk = ch.index_select(1, cm["c0"]).index_select(2, cm["c1"])[..., :cm["k2"]] / float(nc0 * nc1 * nc2)
+            tmp = torch.zeros((C, self.grid.n_glob[0], cm["f1"].numel(), cm["k2"]), dtype=torch.complex128,
+                              device="cuda")
+            tmp.index_copy_(1, cm["f0"], blk)
+            spec[:, :, :, :cm["k2"]].index_copy_(2, cm["f1"], tmp)
+        out = torch.empty((C, *self.grid.n), dtype=torch.float64, device="cuda")
+        return self.fft.inverse(spec, out)
+
+    def _coarse_ops(self):
+        if getattr(self, "_coarse", None) is None or self._coarse[0] is not self.mseries[-1]:
+            cm = self._coarse_maps()
+            mc = self._restrict(self.mseries[-1].unsqueeze(0))[0].contiguous()
+            gc = torch.empty((3, *cm["nc"]), dtype=torch.float64, device="cuda")
+            L.check(L.lib().frg_fd8_gradient(L.n3(cm["nc"]), 3, L.F64, 1, _c(mc), _c(gc), L.stream()), "fd8_coarse")
+            self._coarse = (self.mseries[-1], gc)
+        return self._coarse[1]
+
+    def _coarse_inv_sqrt(self, w: torch.Tensor) -> torch.Tensor:
+        cm = self._coarse_maps()
+        out = torch.empty_like(w)
+        L.check(L.lib().frg_spectral_apply(L.n3(cm["nc"]), 3, L.F64, 3, _c(w), _c(out), L.SYM["reg_inv_sqrt"],
+                                           ctypes.byref(self._reg), L.stream()), "coarse_inv_sqrt")
+        return out
+
+    def _two_level(self, r: torch.Tensor, kind: PrecondKind, outer_tol: float):
+        """kkt.py:325-341; None on a coarse PCG breakdown (caller falls back)."""
+        u = self.fft.apply(r, "reg_inv_sqrt", self._reg)
+        u_low = self._restrict(u)  # restrict(low_pass(u)) == restrict(u): both keep |k_i| < n_i/4
+        gc = self._coarse_ops()
+
+        def op(w):  # kkt.py:297-306: w + R^-1/2 ((g_c . R^-1/2 w) g_c)
+            sw = self._coarse_inv_sqrt(w)
+            return w + self._coarse_inv_sqrt((gc * sw).sum(0) * gc)
+
+        sol, broke = self._pcg_local(op, u_low, kind.inner_tol_factor * outer_tol, kind.inner_max_iterations)
+        if broke:
+            return None
+        s = self._prolong(sol) + self.fft.apply(u, "highpass", self._reg)  # low_pass(prolong(.)) == prolong(.)
+        return self.fft.apply(s, "reg_inv_sqrt", self._reg)
+
+    @staticmethod
+    def _pcg_local(apply_op, rhs: torch.Tensor, tol_rel: float, max_it: int):
+        """kkt.py:99-133 with the identity preconditioner on a replicated
+        coarse problem (rank-local inner products, identical on every rank)."""
+        dot = lambda a, b: float((a * b).sum())  # noqa: E731
+        x = torch.zeros_like(rhs)
+        r = rhs.clone()
+        rhs_norm = math.sqrt(max(dot(rhs, rhs), 0.0))
+        if rhs_norm == 0.0:
+            return x, False
+        s = r.clone()
+        rz = dot(r, r)
+        it = 0
+        while it < max_it:
+            op_s = apply_op(s)
+            s_op_s = dot(s, op_s)
+            if not math.isfinite(s_op_s) or s_op_s <= 0.0:
+                return x, True
+            kappa = rz / s_op_s
+            x.add_(s, alpha=kappa)
+            r.add_(op_s, alpha=-kappa)
+            it += 1
+            if math.sqrt(max(dot(r, r), 0.0)) <= tol_rel * rhs_norm:
+                break
+            rz_new = dot(r, r)
+            if not math.isfinite(rz_new) or rz_new <= 0.0:
+                return x, True
+            mu = rz_new / rz
+            rz = rz_new
+            s = r.clone().add_(s, alpha=mu)
+        return x, False
+
+    def _apply_h0(self, s64: torch.Tensor) -> torch.Tensor:
+        """kkt.py:275-289: alpha L (zero symbol -> 1) s + (grad m(1) . s) grad m(1),
+        grad = FD8 of the deformed image (the refresh's last gradient slice)."""
+        if self._h0_grad is None:
+            self._h0_grad = self.grads[self.grid.n_t].to(torch.float64)
+        gm = self._h0_grad
+        out = self.fft.apply(s64, "reg_kc", self._reg)
+        out += (gm * s64).sum(0) * gm
+        return out
+
+    def _inner_pcg(self, apply_op, rhs: torch.Tensor, tol_rel: float, max_it: int):
+        """kkt.py:99-133 with global (all-reduced) inner products; 'reg'
+        preconditioned.  Returns (solution, breakdown)."""
+        x = torch.zeros_like(rhs)
+        r = rhs.clone()
+        rhs_norm = math.sqrt(max(self.dot(rhs, rhs), 0.0))
+        if rhs_norm == 0.0:
+            return x, False
+        z = self.fft.apply(r, "reg_inv", self._reg)
+        s = z.clone()
+        rz = self.dot(r, z)
+        it = 0
+        while it < max_it:
+            op_s = apply_op(s)
+            s_op_s = self.dot(s, op_s)
+            if not math.isfinite(s_op_s) or s_op_s <= 0.0:
+                return x, True
+            kappa = rz / s_op_s
+            x.add_(s, alpha=kappa)
+            r.add_(op_s, alpha=-kappa)
+            it += 1
+            if math.sqrt(max(self.dot(r, r), 0.0)) <= tol_rel * rhs_norm:
+                break
+            z = self.fft.apply(r, "reg_inv", self._reg)
+            rz_new = self.dot(r, z)
+            if not math.isfinite(rz_new) or rz_new <= 0.0:
+                return x, True
+            mu = rz_new / rz
+            rz = rz_new
+            s = z.add_(s, alpha=mu)
+        return x, False
 
     def _reg_energy(self, v64: torch.Tensor) -> float:
         lv = self.fft.apply(v64.to(self._spec_dt), "reg", self._reg).to(torch.float64)
@@ -691,7 +929,7 @@ class DistKktState:
 
     def objective(self) -> float:
         if self._dist is None:
-            self._dist = self._ssd(self.mseries[-1])
+            self._dist = self._dist_value(self.mseries[-1])
         return self._dist + self._reg_energy(self.v.data)
 
     def objective_at(self, v_trial) -> float:
@@ -702,13 +940,13 @@ class DistKktState:
         m = self._state_solve(disp, self._halo_of(disp), keep=False)
         self._bind()
         self.pde_solves += 1
-        return self._ssd(m) + self._reg_energy(vt)
+        return self._dist_value(m) + self._reg_energy(vt)
 
     def mismatch(self) -> float:
         if self._init_mismatch == 0.0:
             return 0.0
         if self._dist is None:
-            self._dist = self._ssd(self.mseries[-1])
+            self._dist = self._dist_value(self.mseries[-1])
         return self._dist / self._init_mismatch
 
     def divergence_energy(self) -> float:
@@ -764,14 +1002,16 @@ class DistKktState:
 
 
 def dist_register(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, config=None, reg: RegConfig | None = None,
-                  n_t: int = 4, method: str = "cubic", v0: torch.Tensor | None = None, compute_detgrad: bool = True):
+                  n_t: int = 4, method: str = "cubic", v0: torch.Tensor | None = None, compute_detgrad: bool = True,
+                  distance: str = "ssd", precond: PrecondKind | None = None):
     """optimizer.register (optimizer.py:174-281) on the slab decomposition:
-    the same host control, SPMD on every rank, reductions all-reduced."""
+    the same host control, SPMD on every rank, reductions all-reduced
+    (SSD / NCC; 'reg' or 'h0' preconditioner)."""
     from .optimizer import OptimizerConfig, solve
 
     reg = reg or RegConfig()
-    state = DistKktState(m0, m1, reg, comm, n_glob, n_t=n_t, method=method, v_init=v0)
-    return solve(state, config or OptimizerConfig(), PrecondKind("reg"), compute_detgrad=compute_detgrad)
+    state = DistKktState(m0, m1, reg, comm, n_glob, n_t=n_t, method=method, v_init=v0, distance=distance)
+    return solve(state, config or OptimizerConfig(), precond or PrecondKind("reg"), compute_detgrad=compute_detgrad)
 
 
 def dist_search_alpha(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, cfg=None,

@@ -209,6 +209,78 @@ def test_slab_peer_mode_reaches_past_the_slab(tmp_path):
         assert res["objective"] < 1e-6, res
 
 
+def _worker_ncc_h0(rank, size, port, n, outdir):
+    """NCC distance (distance.py:34-91, global moments all-reduced) and the
+    'h0' preconditioner (kkt.py:269-324, nested PCG with all-reduced inner
+    products) on the slab vs the single-GPU context."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=size)
+    import paper_2401_17493_b200 as F
+    from paper_2401_17493_b200 import dist as D
+
+    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3)
+    reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    v = 0.5 * vtrue.data
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    vt = 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=torch.float64, device="cuda")
+    comm = D.SlabComm()
+    lo, hi = D.slab_bounds(n, size, rank)
+    res = {}
+    ref = F.KktState(m0, m1, reg, distance="ncc", v_init=F.VectorField._wrap(m0.grid, v), transport_dtype=np.float32)
+    st = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
+                        v_init=v[:, lo:hi].contiguous(), distance="ncc")
+    res["ncc_gradient"] = _rel(st.gradient().data, ref.gradient().data[:, lo:hi])
+    res["ncc_matvec"] = _rel(st.hessian_matvec(vt[:, lo:hi].contiguous()).data,
+                             ref.hessian_matvec(F.VectorField._wrap(m0.grid, vt)).data[:, lo:hi])
+    res["ncc_objective"] = abs(st.objective() - ref.objective()) / abs(ref.objective())
+    res["ncc_mismatch"] = abs(st.mismatch() - ref.mismatch())
+    ref_s = F.KktState(m0, m1, reg, v_init=F.VectorField._wrap(m0.grid, v), transport_dtype=np.float32)
+    st_s = D.DistKktState(m0.values[lo:hi].float(), m1.values[lo:hi].float(), reg, comm, (n, n, n),
+                          v_init=v[:, lo:hi].contiguous())
+    pk = F.PrecondKind("h0")
+    res["h0"] = _rel(st_s.apply_precond(vt[:, lo:hi].contiguous(), pk, 0.1).data,
+                     ref_s.apply_precond(F.VectorField._wrap(m0.grid, vt), pk, 0.1).data[:, lo:hi])
+    res["h0_fallbacks"] = [st_s.precond_fallbacks, ref_s.precond_fallbacks]
+    pk2 = F.PrecondKind("2level")
+    res["2level"] = _rel(st_s.apply_precond(vt[:, lo:hi].contiguous(), pk2, 0.1).data,
+                         ref_s.apply_precond(F.VectorField._wrap(m0.grid, vt), pk2, 0.1).data[:, lo:hi])
+    # the reference default (kkt.py:84): a full SPMD solve with the two-level preconditioner
+    from paper_2401_17493_b200.optimizer import OptimizerConfig
+
+    cfg = OptimizerConfig()
+    _, rep_d = D.dist_register(m0.values[lo:hi].float(), m1.values[lo:hi].float(), comm, (n, n, n), config=cfg,
+                               reg=reg, precond=pk2, compute_detgrad=False)
+    _, rep_1 = F.register(m0, m1, config=cfg, reg=reg, precond=pk2, transport_dtype=np.float32,
+                          compute_detgrad=False)
+    res["register_2level"] = {"dist": [rep_d.iterations, rep_d.matvecs, rep_d.status, rep_d.precond_fallbacks],
+                              "single": [rep_1.iterations, rep_1.matvecs, rep_1.status, rep_1.precond_fallbacks],
+                              "mismatch": [rep_d.mismatch, rep_1.mismatch]}
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as fh:
+        json.dump(res, fh)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_slab_ncc_h0_2level_match_single_gpu(tmp_path):
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_worker_ncc_h0, args=(2, _free_port(), 64, str(tmp_path)), nprocs=2, start_method="spawn",
+                       join=True)
+    for r in range(2):
+        res = json.load(open(os.path.join(tmp_path, f"rank{r}.json")))
+        for key in ("ncc_gradient", "ncc_matvec", "h0", "2level"):
+            assert res[key] < 1e-5, (r, key, res[key])
+        assert res["ncc_objective"] < 1e-6 and res["ncc_mismatch"] < 1e-6, res
+        assert res["h0_fallbacks"][0] == res["h0_fallbacks"][1], res
+        reg2 = res["register_2level"]
+        assert reg2["dist"] == reg2["single"], reg2
+        assert abs(reg2["mismatch"][0] - reg2["mismatch"][1]) < 1e-5 * max(reg2["mismatch"][1], 1e-3), reg2
+
+
 @pytest.mark.parametrize("method", ["bspline", "linear"])
 def test_slab_kkt_methods_match_single_gpu(method, tmp_path):
     """B-spline on the slab: global prefilter through the slab FFT, exchanged
