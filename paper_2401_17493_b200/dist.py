@@ -1015,7 +1015,8 @@ def dist_register(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, co
 
 
 def dist_search_alpha(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, cfg=None,
-                      reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic"):
+                      reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic",
+                      distance: str = "ssd", precond: PrecondKind | None = None):
     """continuation.search_alpha (continuation.py:87-207) on the slab
     decomposition: the same sweep / bisection (continuation.run_search), every
     trial a SPMD dist_register warm-started from the previous trial unless the
@@ -1035,11 +1036,12 @@ def dist_search_alpha(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob
         reg_a = replace(reg, alpha=alpha)
         v0, warm_started, dropped = (None if v_warm is None else v_warm.data), v_warm is not None, False
         if v_warm is not None:  # continuation.py:98-108: drop a warm start worse than v = 0
-            st = DistKktState(m0, m1, reg_a, comm, n_glob, n_t=n_t, method=method, v_init=v0)
+            st = DistKktState(m0, m1, reg_a, comm, n_glob, n_t=n_t, method=method, v_init=v0, distance=distance)
             if st.objective() > st._init_mismatch:
                 v0, warm_started, dropped = None, False, True
             del st
-        v, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=reg_a, n_t=n_t, method=method, v0=v0)
+        v, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=reg_a, n_t=n_t, method=method, v0=v0,
+                               distance=distance, precond=precond)
         ok = rep.detgrad_min > cfg.eps_det and rep.detgrad_max < 1.0 / cfg.eps_det
         rec = TrialRecord(alpha=alpha, passed=ok, det_min=rep.detgrad_min, det_max=rep.detgrad_max,
                           det_mean=rep.detgrad_mean, mismatch=rep.mismatch, iterations=rep.iterations,
@@ -1056,7 +1058,8 @@ def dist_search_alpha(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob
 
 
 def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, n_glob, alpha_target: float,
-                            reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic"):
+                            reg: RegConfig | None = None, opt=None, n_t: int = 4, method: str = "cubic",
+                            distance: str = "ssd", precond: PrecondKind | None = None):
     """continuation.continuation_solve (continuation.py:239-293) on the slab
     decomposition — config C5's alpha cascade 1, 0.1, ..., alpha_target with
     warm starts, every stage a SPMD dist_register.  Returns (velocity slab,
@@ -1073,7 +1076,8 @@ def dist_continuation_solve(m0: torch.Tensor, m1: torch.Tensor, comm: SlabComm, 
     alphas = cascade_alphas(alpha_target)
     for a in alphas:
         vv, rep = dist_register(m0, m1, comm, n_glob, config=opt, reg=replace(reg, alpha=a), n_t=n_t, method=method,
-                                v0=None if v is None else v.data, compute_detgrad=(a == alphas[-1]))
+                                v0=None if v is None else v.data, compute_detgrad=(a == alphas[-1]),
+                                distance=distance, precond=precond)
         v = vv
         stages.append(rep)
         total.iterations += rep.iterations
