@@ -319,14 +319,21 @@ __device__ __forceinline__ void stage_fixed(float* __restrict__ box, const float
 #ifndef FRG_SL_DB
 #define FRG_SL_DB 0  // measured: 2 CTAs/SM with two 48 KB boxes lose more than the overlap gains
 #endif
-template <int NF>
+// Ops whose TMA-fed tile epilogue is prefetched into a second box-sized
+// buffer while the gathers run (Op::kEarlyEpilogue, IncFirstOp)
+template <class Op, class = void>
+struct EarlyEpi : std::false_type {};
+template <class Op>
+struct EarlyEpi<Op, std::void_t<decltype(Op::kEarlyEpilogue)>> : std::bool_constant<Op::kEarlyEpilogue> {};
+
+template <int NF, bool EARLY = false>
 struct SlfSmem {
     // one 48 KB box per CTA for single-field steps (4 CTAs / SM); multi-field
     // gathers double-buffer (the next field's TMA overlaps this field's taps)
     static constexpr int NB = (NF > 1 && FRG_SL_DB) ? 2 : 1;
     // + 1 KB: the dynamic window is re-aligned to 1024 B in the kernel (the
     // compiler-placed start after the static shared variables is not)
-    static constexpr size_t bytes = (size_t)NB * TB_VOL * sizeof(float) + 1024;
+    static constexpr size_t bytes = (size_t)(NB + (EARLY ? 1 : 0)) * TB_VOL * sizeof(float) + 1024;
 };
 
 // Ops may take the whole per-thread tile in one epilogue call (done_tile)
@@ -505,7 +512,10 @@ template <class Op>
 struct LateDisp<Op, std::void_t<decltype(Op::kLateDisp)>> : std::bool_constant<Op::kLateDisp> {};
 
 template <int M, int NF, class Op, bool PEER>
-__global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB : FRG_SLF_MINB_MF))
+__global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB
+                                                   : (EarlyEpi<Op>::value     ? 2
+                                                      : SlfSmem<NF>::NB == 2 ? FRG_SLF_MINB_DB
+                                                                             : FRG_SLF_MINB_MF))
     k_slf(Dims g, const __grid_constant__ Op op, const __grid_constant__ TmaMaps<NF> maps, int use_tma,
           const __grid_constant__ PeerArg<PEER> pp) {
     static_assert(M == LINEAR || M == CUBIC || M == BSPLINE, "k_slf: linear / cubic / B-spline only");
@@ -567,13 +577,16 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
         S0 = pe.w & 1023;
         S1 = (pe.w >> 10) & 1023;
         S2 = (pe.w >> 20) & 1023;
-        if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
+        if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K) {
             for (int b = 0; b < NB; ++b) {
                 if constexpr (PEER)
                     tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
                 else
                     tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
             }
+            if constexpr (EarlyEpi<Op>::value)
+                op.prefetch_epilogue(sbox + NB * TB_VOL, &bars[NB], make_int3(blockIdx.x * BX, blockIdx.y * BY, i_base));
+        }
         // no CTA barrier here: the other warps go on with their displacement
         // arithmetic while thread 0 waits for the plan entry and issues the TMA
     }
@@ -630,13 +643,16 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
     S0 = mx0 + Halo<M>::hi - lo0 + 1;
     S1 = mx1 + Halo<M>::hi - lo1 + 1;
     S2 = mx2 + Halo<M>::hi - lo2 + 1;
-    if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K)
+    if (tid == 0 && use_tma && S0 <= TB_I && S1 <= TB_J && S2 <= TB_K) {
         for (int b = 0; b < NB; ++b) {
             if constexpr (PEER)
                 tma_box_peer(sbox + b * TB_VOL, pp, b, g, lo0, lo1, lo2, S0, &bars[b]);
             else
                 tma_box(sbox + b * TB_VOL, &maps.m[b], g, lo0, lo1, lo2, S0, &bars[b]);
         }
+        if constexpr (EarlyEpi<Op>::value)
+            op.prefetch_epilogue(sbox + NB * TB_VOL, &bars[NB], make_int3(blockIdx.x * BX, blockIdx.y * BY, i_base));
+    }
     }
     const bool fits = S0 <= TB_I && S1 <= TB_J && S2 <= TB_K;
 
@@ -726,7 +742,8 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB : (SlfSmem<NF>:
             __syncthreads();  // the box is free once every thread is done with the last gather
             op.template done_tile_smem<SL_TI>((i_base * g.n1 + j) * g.n2 + k, g.n1 * g.n2, ok, vals, sbox, tid,
                                               BX * BY, &bars[NB], use_tma,
-                                              make_int3(blockIdx.x * BX, blockIdx.y * BY, i_base));
+                                              make_int3(blockIdx.x * BX, blockIdx.y * BY, i_base),
+                                              EarlyEpi<Op>::value && use_tma ? sbox + NB * TB_VOL : nullptr);
             return;
         }
     }
@@ -775,7 +792,7 @@ void launch_slf(const Dims& g, const Op& op_in, cudaStream_t st) {
         else
             memset(&maps.m[f], 0, sizeof(CUtensorMap));
     }
-    constexpr size_t smem = SlfSmem<NF>::bytes;
+    constexpr size_t smem = SlfSmem<NF, EarlyEpi<Op>::value>::bytes;
     static bool attr_set[2] = {false, false};  // per instantiation
     if (!attr_set[peer]) {
         if (peer)

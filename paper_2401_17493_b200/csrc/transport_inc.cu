@@ -88,6 +88,28 @@ struct IncFirstOp {
     alignas(64) CUtensorMap tm_gy;  // gy as n_t D n0 stacked planes
     alignas(64) CUtensorMap tm_gx;  // gx as (n_t + 1) D n0 stacked planes
     int tma_epi = 0, n0 = 0;
+#ifndef FRG_INC_PREFETCH
+#define FRG_INC_PREFETCH 0
+#endif
+    // round 0 of the TMA epilogue issued with the gather boxes into a second
+    // 48 KB buffer (k_slf, EarlyEpi): 2 CTAs / SM instead of 3.  Measured
+    // slower (matvec 3630 vs 3544 us at 256^3): build option, off
+    static constexpr bool kEarlyEpilogue = FRG_INC_PREFETCH && std::is_same<T, float>::value && D == 3;
+    __device__ __forceinline__ void issue_round(T* buf, uint64_t* ebar, int3 org, int j0, int nj, int nthreads) const {
+        mbar_expect_tx(ebar, (unsigned)(nj * 2 * D * SL_TI * nthreads * sizeof(T)));
+        for (int jj = 0; jj < nj; ++jj) {
+            const int j = j0 + jj;
+            for (int c = 0; c < D; ++c) {
+                tma_load_3d(buf + (size_t)((jj * 2 * D + c) * SL_TI) * nthreads, &tm_gy, org.x, org.y,
+                            (j * D + c) * n0 + org.z, ebar);
+                tma_load_3d(buf + (size_t)((jj * 2 * D + D + c) * SL_TI) * nthreads, &tm_gx, org.x, org.y,
+                            ((j + 1) * D + c) * n0 + org.z, ebar);
+            }
+        }
+    }
+    __device__ __forceinline__ void prefetch_epilogue(T* buf, uint64_t* ebar, int3 org) const {
+        if (tma_epi) issue_round(buf, ebar, org, 0, n_t > 1 ? 2 : 1, BX * BY);
+    }
     __device__ __forceinline__ void disp(int p, T& d0, T& d1, T& d2) const { ds.get(p, d0, d1, d2); }
     __host__ __device__ __forceinline__ const T* field(int f) const { return vtT[f]; }
     void set_field(int f, const T* p) { vtT[f] = p; }
@@ -141,7 +163,7 @@ struct IncFirstOp {
     template <int TI>
     __device__ __forceinline__ void done_tile_smem(int p0, int pstride, const bool (&ok)[TI],
                                                    const T (&vals)[TI][D], T* smem, int tid, int nthreads,
-                                                   uint64_t* ebar, int use_tma, int3 org) const {
+                                                   uint64_t* ebar, int use_tma, int3 org, T* pre_smem = nullptr) const {
         static_assert(sizeof(T) == 4, "smem-staged epilogue is the fp32 path");
         T vx[TI][D];
 #pragma unroll
@@ -153,23 +175,20 @@ struct IncFirstOp {
             if (use_tma && tma_epi) {
                 // box q of a round holds field q's (TI, BY, BX) tile: voxel (u, ty, tx) at
                 // u * 256 + tid == slot(q, u), the layout the cp.async path writes
+                const bool pre = pre_smem != nullptr && tma_epi;
                 for (int j0 = 0, r = 0; j0 < n_t; j0 += 2, ++r) {
                     const int nj = (j0 + 1 < n_t) ? 2 : 1;
-                    if (r > 0) __syncthreads();  // every thread is done with the previous round's boxes
-                    if (tid == 0) {
-                        fence_proxy_async();
-                        mbar_expect_tx(ebar, (unsigned)(nj * 2 * D * TI * nthreads * sizeof(T)));
-                        for (int jj = 0; jj < nj; ++jj) {
-                            const int j = j0 + jj;
-                            for (int c = 0; c < D; ++c) {
-                                tma_load_3d(slot(jj * 2 * D + c, 0) - tid, &tm_gy, org.x, org.y,
-                                            (j * D + c) * n0 + org.z, ebar);
-                                tma_load_3d(slot(jj * 2 * D + D + c, 0) - tid, &tm_gx, org.x, org.y,
-                                            ((j + 1) * D + c) * n0 + org.z, ebar);
-                            }
+                    // round 0 may already be in flight in pre_smem (issued with the gather boxes)
+                    T* buf = (pre && r == 0) ? pre_smem : smem;
+                    if (!(pre && r == 0)) {
+                        if (r > 0 && !(pre && r == 1)) __syncthreads();  // the previous round's boxes are consumed
+                        if (tid == 0) {
+                            fence_proxy_async();
+                            issue_round(buf, ebar, org, j0, nj, nthreads);
                         }
                     }
                     mbar_wait_sleep(ebar, (unsigned)(r & 1));
+                    auto slot = [&](int q, int u) -> T* { return buf + ((size_t)(q * TI + u) * nthreads + tid); };
                     for (int jj = 0; jj < nj; ++jj) {
                         const int j = j0 + jj;
 #pragma unroll
