@@ -150,6 +150,7 @@ struct KktCtx {
     int interp_bits = 32;           // 16: fp16-tap SL steps (mixed-precision interpolation mode)
     // two-level coarse pieces
     DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
+    DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
     bool coarse_ready = false, h0_ready = false;
     bool have_images = false, have_state = false;
     double initial_mismatch = 0.0, dist_cur = 0.0;
@@ -231,7 +232,7 @@ void kkt_destroy(KktCtx* k) {
                       &k->mseries, &k->grads, &k->grads_y, &k->lam, &k->vtT, &k->vty, &k->mt, &k->lt, &k->bf,
                       &k->disp_trial, &k->mtrial, &k->gmC, &k->tmp1, &k->tmp2, &k->tmp3, &k->c_gm, &k->c_w,
                       &k->c_x, &k->c_r, &k->c_z, &k->c_s, &k->c_q, &k->c_u, &k->plan_f, &k->plan_b,
-                      &k->plan_t};
+                      &k->plan_t, &k->pre32};
     for (DevBuf* b : bufs) b->free_();
     k->g_in.free_();
     k->g_out.free_();
@@ -706,8 +707,25 @@ void kkt_apply_precond(KktCtx* k, int kind, double outer_tol, double inner_tol_f
     const Dims& g = k->g;
     const long long dN = (long long)g.d * g.N;
     const size_t C = k->C();
-    if (kind == 0) {
-        apply_sym_c(k, g, r, z, SK_REG_INV);  // kkt.py:310-311
+    if (kind == 0) {  // kkt.py:310-311
+        // mixed mode: (alpha L)^-1 damps every nonzero mode (1 / (alpha |k|^2)),
+        // so the fp32 transforms' rounding, ~1e-7 of |r| in every bin, stays
+        // ~1e-7 of |z| (unlike alpha L, whose amplification forces the f64
+        // forward transform of the matvec, §6 of DESIGN.md): fp32 R2C / C2R
+        // bracketed by one narrowing and one widening pass, 1.14 -> ~0.6 ms
+        // per call at 256^3
+        static const bool f64_pre = getenv("FRG_F64_PRECOND") != nullptr;
+        if (k->tdt == F32 && k->cdt == F64 && !f64_pre) {
+            k->pre32.alloc(2 * dN * sizeof(float));
+            float* in32 = k->pre32.at<float>();
+            float* out32 = in32 + dN;
+            convert(F64, r, F32, in32, dN, k->st);
+            size_t need = spectral_ws_bytes(g, F32, g.d);
+            spectral_apply_ex(k->plans, k->ws_c.get(need), g, F32, g.d, in32, out32, SK_REG_INV, k->reg, k->st);
+            convert(F32, out32, F64, z, dN, k->st);
+            return;
+        }
+        apply_sym_c(k, g, r, z, SK_REG_INV);
         return;
     }
     double tol = inner_tol_factor * outer_tol;
