@@ -550,12 +550,31 @@ __global__ void __launch_bounds__(BX* BY, NF == 1 ? FRG_SLF_MINB
     // plan entry), so the CTA pays one memory latency, not three in a row
     bool ok[SL_TI];
     float dsp[SL_TI][3];
+    if constexpr (HasDs<Op>::value) {
+        // the map's component pointers and the column offset once per thread
+        // (DispSrc::get per voxel re-derived them under each voxel's predicate)
+        const int plane = g.n1 * g.n2, p0 = (i_base * g.n1 + j) * g.n2 + k;
+        const float* __restrict__ a0 = op.ds.a[0];
+        const float* __restrict__ a1 = op.ds.a[1] + p0;
+        const float* __restrict__ a2 = op.ds.a[2] + p0;
 #pragma unroll
-    for (int u = 0; u < SL_TI; ++u) {
-        const int i = i_base + u;
-        ok[u] = in_kj && i < g.n0;
-        dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
-        if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, dsp[u][0], dsp[u][1], dsp[u][2]);
+        for (int u = 0; u < SL_TI; ++u) {
+            ok[u] = in_kj && i_base + u < g.n0;
+            dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
+            if (ok[u]) {
+                dsp[u][0] = a0 ? __ldg(a0 + p0 + u * plane) : 0.f;
+                dsp[u][1] = __ldg(a1 + u * plane);
+                dsp[u][2] = __ldg(a2 + u * plane);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < SL_TI; ++u) {
+            const int i = i_base + u;
+            ok[u] = in_kj && i < g.n0;
+            dsp[u][0] = dsp[u][1] = dsp[u][2] = 0.f;
+            if (ok[u]) op.disp((i * g.n1 + j) * g.n2 + k, dsp[u][0], dsp[u][1], dsp[u][2]);
+        }
     }
     // the gathered sources and epilogue inputs may be the predecessor's outputs
     if constexpr (!LateDisp<Op>::value) griddep_wait();
