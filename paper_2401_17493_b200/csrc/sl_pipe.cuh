@@ -55,7 +55,7 @@ constexpr int PIPE_SLOTS = PIPE_GSLOTS * PIPE_GROUPS;
 constexpr int PB_I = FRG_PB_I, PB_J = FRG_PB_J, PB_K = FRG_PB_K;
 constexpr int PB_PLANE = PB_J * PB_K, PB_VOL = PB_I * PB_PLANE;
 static_assert(PB_PLANE % 32 == 0, "TMA destinations (box planes) must be 128-byte aligned");
-static_assert(PB_K % 4 == 0 && PB_K <= TB_K && PB_J <= TB_J, "pipeline box within the TMA box limits");
+static_assert(PB_K % 4 == 0 && PB_K <= 256 && PB_J <= 256, "pipeline box within the TMA box limits");
 
 struct SlpSmem {
     static constexpr size_t bytes = (size_t)PIPE_SLOTS * PB_VOL * sizeof(float) + 1024;
