@@ -151,6 +151,7 @@ struct KktCtx {
     // two-level coarse pieces
     DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
     DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
+    bool gy_ready = false;  // grads_y (grad m_j at the forward feet) matches the current state
     bool coarse_ready = false, h0_ready = false;
     bool have_images = false, have_state = false;
     double initial_mismatch = 0.0, dist_cur = 0.0;
@@ -374,16 +375,10 @@ void kkt_refresh(KktCtx* k, const void* v) {
     FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
     solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);         // kkt.py:174
     gradient_slices(k, k->n_t + 1, k->mseries.p, k->grads.p);                              // kkt.py:175
-    {
-        // grad m_j at the forward feet, reused by every matvec (transport.py:172)
-        std::vector<const void*> in(d * k->n_t);
-        std::vector<void*> out(d * k->n_t);
-        for (long long e = 0; e < d * k->n_t; ++e) {
-            in[e] = k->grads.at<char>(e * N * T);
-            out[e] = k->grads_y.at<char>(e * N * T);
-        }
-        gather_fields(k->g, k->tdt, k->method, k->disp_f.p, (int)(d * k->n_t), in.data(), out.data(), st);
-    }
+    // grad m_j at the forward feet (transport.py:172) is only read by the GN
+    // matvec: gathered by its first call after this refresh (ensure_grads_y),
+    // so the refresh that ends a solve — no matvec follows — skips it
+    k->gy_ready = false;
     adjoint_multiplier(k->g, k->tdt, k->method, 1.0 / k->n_t, k->disp_b.p, k->divv.p, k->cmul.p, st);
     void* m_final = k->mseries.at<char>((size_t)k->n_t * N * T);
     void* lam_final = k->lam.at<char>((size_t)k->n_t * N * T);
@@ -397,6 +392,22 @@ void kkt_refresh(KktCtx* k, const void* v) {
 }
 
 static const void* m_final(KktCtx* k) { return k->mseries.at<char>((size_t)k->n_t * k->N() * k->T()); }
+
+// grad m_j gathered at the forward feet for the incremental state solve; once per refresh
+static void ensure_grads_y(KktCtx* k) {
+    if (k->gy_ready) return;
+    const long long N = k->N(), d = k->g.d;
+    const size_t T = k->T();
+    PlanScope pf(0, k->disp_f.p, plan_of(k, k->plan_f), k->method);
+    std::vector<const void*> in(d * k->n_t);
+    std::vector<void*> out(d * k->n_t);
+    for (long long e = 0; e < d * k->n_t; ++e) {
+        in[e] = k->grads.at<char>(e * N * T);
+        out[e] = k->grads_y.at<char>(e * N * T);
+    }
+    gather_fields(k->g, k->tdt, k->method, k->disp_f.p, (int)(d * k->n_t), in.data(), out.data(), k->st);
+    k->gy_ready = true;
+}
 
 static double current_dist(KktCtx* k) {
     if (!k->dist_valid) {
@@ -538,6 +549,7 @@ static std::vector<const void*> graph_key(KktCtx* k) {
 
 void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
     FRG_REQUIRE(k->have_state, "refresh first");
+    ensure_grads_y(k);  // eager, never inside the small-grid graph capture
     const size_t bytes = (size_t)k->g.d * k->N() * k->C();
     if (graph_ok(k) && ++k->mv_calls >= 2) {  // the first call allocates every workspace the sequence uses
         k->g_in.alloc(bytes);
