@@ -109,6 +109,9 @@ static void pool_put(void* p, size_t b) {
 }
 
 void kkt_release_pool() { pool_release_all(); }
+// spectral workspaces (spectral.h) recycle through the same pool
+void* pool_alloc(size_t& bytes) { return pool_get(bytes); }
+void pool_free(void* p, size_t bytes) { pool_put(p, bytes); }
 
 struct DevBuf {
     void* p = nullptr;

@@ -19,6 +19,11 @@ struct PlanCache {
     ~PlanCache();
 };
 
+// process-wide device buffer pool (kkt.cu): callers guarantee no queued work
+// still uses a buffer they hand back
+void* pool_alloc(size_t& bytes);
+void pool_free(void* p, size_t bytes);
+
 struct Workspace {
     void* ptr = nullptr;
     size_t cap = 0;

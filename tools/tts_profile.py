@@ -17,10 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=256)
 ap.add_argument("--precond", default="reg")
 ap.add_argument("--incomp", default="near-incompressible")
+ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
 
 acc = collections.defaultdict(float)
 cnt = collections.Counter()
+mx = collections.defaultdict(float)
 
 
 def wrap(name):
@@ -31,8 +33,10 @@ def wrap(name):
         t = time.perf_counter()
         r = f(self, *args, **kw)
         torch.cuda.synchronize()
-        acc[name] += time.perf_counter() - t
+        dt = time.perf_counter() - t
+        acc[name] += dt
         cnt[name] += 1
+        mx[name] = max(mx[name], dt)
         return r
     setattr(kkt.KktState, name, g)
 
@@ -43,9 +47,10 @@ for nm in ["__init__", "refresh", "gradient", "hessian_matvec", "apply_precond",
 
 m0, m1, v = F.synth_case("rotation", a.n, seed=1, d=3)
 reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode(a.incomp, 1e-4))
-for rep in range(2):
+for rep in range(a.reps):
     acc.clear()
     cnt.clear()
+    mx.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     vs, r = F.register(m0, m1, reg=reg, precond=F.PrecondKind(a.precond), transport_dtype=np.float32)
@@ -53,4 +58,4 @@ for rep in range(2):
     wall = time.perf_counter() - t0
     print(f"run {rep}: wall {wall:.3f}s it={r.iterations} mv={r.matvecs} status={r.status}")
     for k in sorted(acc, key=lambda k: -acc[k]):
-        print(f"   {k:18s} {cnt[k]:4d} calls {acc[k]*1e3:9.1f} ms")
+        print(f"   {k:18s} {cnt[k]:4d} calls {acc[k]*1e3:9.1f} ms  (max {mx[k]*1e3:.2f} ms)")
