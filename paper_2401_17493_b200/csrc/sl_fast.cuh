@@ -247,14 +247,24 @@ __device__ __forceinline__ void patch_axis_f(float* __restrict__ box, const Plan
     const int b_beg = lo + S > n ? max(n - lo, 0) : S;
     const int cnt = a_end + (S - b_beg);
     if (cnt == 0) return;
-    // the two other extents
+    // the two other extents; the column patch (axis 2, after axis 1) skips the
+    // rows the row patch already wrote (no duplicate writes of the corners)
     const int E1 = axis == 0 ? S1 : S0;           // outer of the remaining pair
-    const int E2 = axis == 2 ? S1 : S2;           // inner of the remaining pair
+    int E2 = axis == 2 ? S1 : S2;                 // inner of the remaining pair
+    int r0 = 0;
+    if (axis == 2) {
+        r0 = lo1 < 0 ? min(-lo1, S1) : 0;
+        E2 = (lo1 + S1 > g.n1 ? max(g.n1 - lo1, 0) : S1) - r0;
+        if (E2 <= 0) return;
+    }
     const int total = cnt * E1 * E2;
+    // multiply-high division (exact below 2^16: every TB box; the pipe engine's larger boxes divide)
+    const bool magic = total < 65536;
+    const unsigned m2 = div_magic((unsigned)E2), m1 = div_magic((unsigned)E1);
     for (int e = tid; e < total; e += nthreads) {
-        int r = e / E2;
+        int r = magic ? (int)fast_div((unsigned)e, m2) : e / E2;
         const int in2 = e - r * E2;
-        const int q = r / E1;
+        const int q = magic ? (int)fast_div((unsigned)r, m1) : r / E1;
         const int in1 = r - q * E1;
         const int x = q < a_end ? q : b_beg + (q - a_end);
         int a, b, c;
@@ -263,7 +273,7 @@ __device__ __forceinline__ void patch_axis_f(float* __restrict__ box, const Plan
         } else if (axis == 1) {
             a = in1; b = x; c = in2;
         } else {
-            a = in1; b = in2; c = x;
+            a = in1; b = r0 + in2; c = x;
         }
         const int gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
         cp_async_elem<4>(box + (a * J + b) * K + c, plane_of(lo0 + a) + (gj * g.n2 + gk));
@@ -281,12 +291,21 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
     const int cnt = a_end + (S - b_beg);
     if (cnt == 0) return;
     const int E1 = axis == 0 ? S1 : S0;
-    const int E2 = axis == 2 ? S1 : S2;
+    int E2 = axis == 2 ? S1 : S2;
+    int r0 = 0;
+    if (axis == 2) {  // rows outside [0, n1) were written by the axis-1 patch
+        r0 = lo1 < 0 ? min(-lo1, S1) : 0;
+        E2 = (lo1 + S1 > g.n1 ? max(g.n1 - lo1, 0) : S1) - r0;
+        if (E2 <= 0) return;
+    }
     const int total = cnt * E1 * E2;
+    // multiply-high division (exact below 2^16: every TB box; the pipe engine's larger boxes divide)
+    const bool magic = total < 65536;
+    const unsigned m2 = div_magic((unsigned)E2), m1 = div_magic((unsigned)E1);
     for (int e = tid; e < total; e += nthreads) {
-        int r = e / E2;
+        int r = magic ? (int)fast_div((unsigned)e, m2) : e / E2;
         const int in2 = e - r * E2;
-        const int q = r / E1;
+        const int q = magic ? (int)fast_div((unsigned)r, m1) : r / E1;
         const int in1 = r - q * E1;
         const int x = q < a_end ? q : b_beg + (q - a_end);
         int a, b, c;
@@ -295,7 +314,7 @@ __device__ __forceinline__ void patch_axis(float* __restrict__ box, const float*
         } else if (axis == 1) {
             a = in1; b = x; c = in2;
         } else {
-            a = in1; b = in2; c = x;
+            a = in1; b = r0 + in2; c = x;
         }
         const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
         cp_async_elem<4>(box + (a * J + b) * K + c, src + ((gi * g.n1 + gj) * g.n2 + gk));

@@ -86,8 +86,14 @@ __device__ __forceinline__ void patch_axis_half(__half* __restrict__ box, const 
     const int b_beg = lo + S > n ? max(n - lo, 0) : S;
     const int cnt = a_end + (S - b_beg);
     if (cnt == 0) return;
-    const int E1 = S0;                    // planes
-    const int E2 = axis == 2 ? S1 : S2;  // the other in-plane extent
+    const int E1 = S0;              // planes
+    int E2 = axis == 2 ? S1 : S2;  // the other in-plane extent
+    int r0 = 0;
+    if (axis == 2) {  // rows outside [0, n1) were written by the axis-1 patch
+        r0 = lo1 < 0 ? min(-lo1, S1) : 0;
+        E2 = (lo1 + S1 > g.n1 ? max(g.n1 - lo1, 0) : S1) - r0;
+        if (E2 <= 0) return;
+    }
     const int total = cnt * E1 * E2;
     for (int e = tid; e < total; e += BX * BY) {
         const int r = e / E2;
@@ -95,7 +101,7 @@ __device__ __forceinline__ void patch_axis_half(__half* __restrict__ box, const 
         const int q = r / E1;
         const int a = r - q * E1;
         const int x = q < a_end ? q : b_beg + (q - a_end);
-        const int b = axis == 1 ? x : in2, c = axis == 1 ? in2 : x;
+        const int b = axis == 1 ? x : r0 + in2, c = axis == 1 ? in2 : x;
         const int gi = src_plane(g, lo0 + a), gj = wrap_near(lo1 + b, g.n1), gk = wrap_near(lo2 + c, g.n2);
         box[(a * TB_J + b) * TB_K + c] = src[((size_t)gi * g.n1 + gj) * g.n2 + gk];
     }
