@@ -20,7 +20,7 @@ from paper_2401_17493_b200 import _lib as L
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=256)
-ap.add_argument("--what", default="matvec", choices=["matvec", "refresh", "gather", "gradient"])
+ap.add_argument("--what", default="matvec", choices=["matvec", "refresh", "gather", "gradient", "precond", "objective_at", "detgrad"])
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--precision", default="mixed")
 ap.add_argument("--interp", default="fp32", choices=["fp32", "fp16"])
@@ -55,6 +55,12 @@ def step():
         st.gradient()
     elif a.what == "refresh":
         st.refresh(v)
+    elif a.what == "precond":
+        st.apply_precond(vt, F.PrecondKind("reg"), 0.5, out=out)
+    elif a.what == "objective_at":
+        st.objective_at(F.VectorField._wrap(grid, 0.4 * vtrue.data))  # a smooth Armijo trial
+    elif a.what == "detgrad":
+        st.detgrad_stats()
     else:
         L.check(L.lib().frg_gather_planned(L.n3((n, n, n)), 3, 2, ctypes.c_void_p(disp.data_ptr()), L.ptr(plan), 1,
                                            ins, outs, L.stream()), "gather")
