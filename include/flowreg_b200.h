@@ -106,7 +106,6 @@ int frg_points_to_disp(const int32_t n[3], int32_t d, int32_t dtype, const void*
 /* nf scalar fields gathered at x + disp                                     interp.py:42-62 */
 int frg_gather(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, const void* disp, int32_t nf,
                const void* const* in, void* const* out, void* stream);
-/* series[0] holds m0; fills series[1..n_t]                                   transport.py:83-98 */
 /* SL tile plan of an fp32 displacement map (one int4 per 32x8x4 tile: the
  * stencil bounding box), built once per map and reused by every gather on it
  * (frg_gather_planned); the KKT context builds and binds its own plans. */
@@ -116,6 +115,7 @@ int frg_tile_plan(const int32_t n[3], int32_t d, int32_t method, const void* dis
 int frg_gather_planned(const int32_t n[3], int32_t d, int32_t method, const void* disp, const void* plan, int32_t nf,
                        const void* const* in, void* const* out, void* stream);
 
+/* series[0] holds m0; fills series[1..n_t]                                   transport.py:83-98 */
 int frg_solve_state(const int32_t n[3], int32_t d, int32_t dtype, int32_t method, int32_t n_t, const void* disp,
                     void* series, void* stream);
 /* series[n_t] holds the final condition; fills series[0..n_t-1]             transport.py:105-135 */
