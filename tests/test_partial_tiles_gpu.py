@@ -1,10 +1,10 @@
 """The TMA engine on grids whose extents are not multiples of its 32 x 8 x 4
 voxel tiles (even extents, as fields.py:54-80 requires; partial tiles on
 every axis: masked voxels, tile plans of edge tiles, the IncFirst TMA
-epilogue's out-of-range boxes, periodic patches on non-power-of-two axes) against the CPU oracle (oracle/flowreg_oracle.py,
-kkt.py:136-265): mixed precision within the north-star fp32 bar (rel-L2
-1e-5), f64 within 1e-10, and a grid below the TMA box (cp.async staging) for
-the same checks."""
+epilogue's out-of-range boxes, periodic patches on non-power-of-two axes)
+against the CPU oracle (oracle/flowreg_oracle.py, kkt.py:136-265): mixed
+precision within the north-star fp32 bar (rel-L2 1e-5), f64 within 1e-10,
+and a grid below the TMA box (cp.async staging) for the same checks."""
 import os
 import sys
 
