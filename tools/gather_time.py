@@ -51,4 +51,6 @@ gat = timeit(lambda: L.check(L.lib().frg_gather_planned(nn, 3, 2, ctypes.c_void_
 mv = timeit(lambda: st.hessian_matvec(vt, out=out), 20)
 vv = F.VectorField._wrap(m0.grid, 0.5 * vtrue.data)
 rf = timeit(lambda: st.refresh(vv), 10)
-print(f"{os.environ.get('FRG_LIB', 'default')}: gather {gat:.1f} us  matvec {mv:.1f} us  refresh {rf:.1f} us")
+dg = timeit(lambda: st.detgrad_stats(), 5)  # 12 three-field gathers + pointwise updates
+print(f"{os.environ.get('FRG_LIB', 'default')}: gather {gat:.1f} us  matvec {mv:.1f} us  refresh {rf:.1f} us  "
+      f"detgrad {dg:.1f} us")
