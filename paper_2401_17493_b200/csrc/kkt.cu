@@ -861,6 +861,7 @@ void kkt_detgrad(KktCtx* k, double out[3]) {
     det.alloc(N * T);
     // jacobian rows = gradient of each velocity component (diffops.py:132-139)
     gradient_slices(k, (int)d, k->vT.p, jac.p);
+    PlanScope pf(0, k->disp_f.p, plan_of(k, k->plan_f), k->method);  // the F gathers run on the forward map
     deformation_tensor(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, jac.p, F.p, work.p, k->st);
     determinant(k->g, k->tdt, F.p, det.p, k->st);
     double mms[3];

@@ -9,6 +9,7 @@
 // Every SL time step is ONE launch of the shared-memory tiled gather engine
 // (sl_tile.cuh) with the step's pointwise update fused into its epilogue.
 #include "ops.h"
+#include <cstdlib>
 #include "sl_half.cuh"
 
 namespace frg {
@@ -207,6 +208,16 @@ template <typename T>
 static void gather_t(const Dims& g, int method, const T* disp, int nf, const void* const* in, void* const* out,
                      cudaStream_t st) {
     int f = 0;
+    // fp32 fields on a planned map: one launch per field.  The single-field
+    // engine runs 4 CTAs/SM (the 3-field one 3, register-limited) and the
+    // planned TMA needs no bounding-box phase, so re-reading the map per field
+    // costs less than the lost residency (12-field grad m_j(y) gather at 256^3:
+    // 2.16 -> 1.95 ms).  FRG_GATHER_GROUP=3 restores 3-field launches.
+    static const int group = getenv("FRG_GATHER_GROUP") ? atoi(getenv("FRG_GATHER_GROUP")) : 1;
+    if (sizeof(T) == 4 && group == 1 && disp_src(g, disp).plan) {
+        for (; f < nf; ++f) gather_n<T, 1>(g, method, disp, in + f, out + f, st);
+        return;
+    }
     while (nf - f >= 3) {
         gather_n<T, 3>(g, method, disp, in + f, out + f, st);
         f += 3;

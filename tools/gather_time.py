@@ -52,5 +52,13 @@ mv = timeit(lambda: st.hessian_matvec(vt, out=out), 20)
 vv = F.VectorField._wrap(m0.grid, 0.5 * vtrue.data)
 rf = timeit(lambda: st.refresh(vv), 10)
 dg = timeit(lambda: st.detgrad_stats(), 5)  # 12 three-field gathers + pointwise updates
+
+
+def refresh_first_matvec():
+    st.refresh(vv)
+    st.hessian_matvec(vt, out=out)  # + the lazy grad m_j(y) gather (12 fields)
+
+
+rm = timeit(refresh_first_matvec, 10) - rf - mv
 print(f"{os.environ.get('FRG_LIB', 'default')}: gather {gat:.1f} us  matvec {mv:.1f} us  refresh {rf:.1f} us  "
-      f"detgrad {dg:.1f} us")
+      f"detgrad {dg:.1f} us  grads_y {rm:.1f} us")
