@@ -309,6 +309,19 @@ def run_b200(a):
     torch.cuda.synchronize()
     barrier()
     t_e2e = max_over_ranks(x0.elapsed_time(x1)) / 1e3
+    # the same call with no overlap between calls (one PCG iteration's view:
+    # H2D, matvec, D2H, then the host has the result before the next call)
+    lat_steps = 5
+    z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    z0.record(stream)
+    for _ in range(lat_steps):
+        st.hessian_matvec(host_in, out=host_out)
+        st.wait_host_io()
+        torch.cuda.synchronize()  # the host holds this call's result before issuing the next
+    z1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_lat = max_over_ranks(z0.elapsed_time(z1)) / 1e3 / lat_steps
     # the host link's own ceiling for this step: H2D of v~ and D2H of a result
     # at once on two copy streams, no compute
     s_h, s_d = torch.cuda.Stream(), torch.cuda.Stream()
@@ -333,7 +346,10 @@ def run_b200(a):
                             "gbs_per_direction": host_in.numel() * host_in.element_size() / t_link / 1e9,
                             "note": "concurrent pinned H2D + D2H of one step's buffers, no compute"},
            "path": "pinned host v~ -> KktState.hessian_matvec(host tensor) (H2D, C-ABI frg_kkt_hessian_matvec, D2H; "
-                   "copies of neighbouring steps overlap the device work on dedicated copy streams) -> pinned host"}
+                   "copies of neighbouring steps overlap the device work on dedicated copy streams) -> pinned host",
+           "latency": {"value": world / t_lat, "unit": UNIT, "ms_per_call": 1e3 * t_lat, "steps": lat_steps,
+                       "note": "each call's H2D, matvec and D2H complete before the next call (no overlap "
+                               "between calls): the per-iteration view of a host-side PCG"}}
 
     # --- time to solution (C3: register at 256^3, reg preconditioner) --------
     tts = None
@@ -549,6 +565,19 @@ def run_slab(a, F, L, world, rank, local, backend):
     torch.cuda.synchronize()
     barrier()
     t_e2e = max_over_ranks(x0.elapsed_time(x1)) / 1e3
+    # the same call with no overlap between calls (one PCG iteration's view:
+    # H2D, matvec, D2H, then the host has the result before the next call)
+    lat_steps = 5
+    z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    z0.record(stream)
+    for _ in range(lat_steps):
+        st.hessian_matvec(host_in, out=host_out)
+        st.wait_host_io()
+        torch.cuda.synchronize()  # the host holds this call's result before issuing the next
+    z1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_lat = max_over_ranks(z0.elapsed_time(z1)) / 1e3 / lat_steps
 
     # time to solution of the same problem: SPMD dist_register (reg preconditioner)
     tts = None
