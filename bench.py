@@ -697,6 +697,21 @@ PORT_VS_NUMBA = {"numba_reference_c1_register_s_8cores": 10.1, "port_c1_register
                  "source": "BASELINE.md §3 (survey container) and this repo's build container"}
 
 
+def all_host_threads() -> int:
+    """Let the CPU arms use every host thread: torchrun exports
+    OMP_NUM_THREADS=1 to its ranks, which would pin the oracle's OpenMP
+    gathers to one core (scipy.fft takes its worker count explicitly)."""
+    import ctypes
+
+    cores = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    try:  # an OpenMP runtime already initialised in this process keeps its ICV: set it too
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(cores)
+    except OSError:
+        pass
+    return cores
+
+
 def cpu_c1_register():
     """The oracle port's full C1 solve (64^3 rotation, H1, reg precond, cubic, fd8,
     f64) on the host cores — BASELINE.md §2 item 3; synth excluded."""
@@ -718,7 +733,7 @@ def cpu_baseline(a, m0, m1, vtrue, vt):
 
     from oracle import flowreg_oracle as O
 
-    cores = os.cpu_count() or 1
+    cores = all_host_threads()
     M0 = m0.values.double().cpu().numpy()
     M1 = m1.values.double().cpu().numpy()
     V = 0.5 * vtrue.data.double().cpu().numpy()
@@ -746,7 +761,7 @@ def run_reference(a):
     from oracle import flowreg_oracle as O
 
     n = a.n
-    cores = os.cpu_count() or 1
+    cores = all_host_threads()
     # inputs: the oracle's own synth (64-step cubic transport); bounded run
     m0, m1, vtrue = O.synth_case("rotation", n, seed=1, d=3, ref_steps=64)
     st = O.Kkt(m0, m1, O.Reg(alpha=1e-2, incomp="near-incompressible", beta=1e-4), 4, "ssd", "cubic", "fd8",
