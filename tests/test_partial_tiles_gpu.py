@@ -54,3 +54,4 @@ def test_partial_tiles_match_oracle(shape, method):
         g = st.gradient().data.cpu().numpy()
         assert _rel(g, ref_g) < tol, (shape, method, tdt, _rel(g, ref_g))
         assert abs(st.objective() - ref_j) <= 10 * tol * abs(ref_j)
+
