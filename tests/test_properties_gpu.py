@@ -588,3 +588,119 @@ def test_register_warm_start_resumes():
     _, r2 = F.register(m0, m1, reg=plain(1e-2), precond=F.PrecondKind("h0"), v0=v)
     assert r2.trace[0]["objective"] == pytest.approx(r1.trace[-1]["objective"], rel=1e-12)
     assert r2.mismatch <= r1.mismatch * 1.05
+
+
+def test_pcg_residual_meets_the_forcing_tolerance():
+    m0, m1, _ = F.synth_case("rotation", 32, seed=2)
+    st = F.KktState(m0, m1, plain(1e-2))
+    grad = st.gradient()
+    vt, _, info = pcg_newton_step(st, grad, F.PrecondKind("reg"), 0.1)
+    res = F.VectorField._wrap(st.grid, st.hessian_matvec(vt).data + grad.data)
+    assert F.norm_l2(res) <= 0.1 * F.norm_l2(grad)
+    assert info["flag"] == "converged"
+
+
+class _Quadratic:
+    """J(v) = 0.5 |v|^2: the slice of the state API the line search uses."""
+
+    def __init__(self, g, v):
+        self.grid, self.v = g, v
+
+    def objective(self):
+        return 0.5 * F.l2_inner(self.v, self.v)
+
+    def objective_at(self, v):
+        return 0.5 * F.l2_inner(v, v)
+
+
+def test_armijo_full_step_and_backtracking_on_a_quadratic(rng):
+    from paper_2401_17493_b200.optimizer import OptimizerConfig
+
+    g = F.Grid((16, 16), n_t=1)
+    model = _Quadratic(g, F.VectorField(g, rng.standard_normal((2, *g.n))))
+    grad = model.v
+    gamma, trials, _ = armijo_line_search(model, F.VectorField._wrap(g, -grad.data), grad)
+    assert gamma == 1.0 and trials == 1
+    cfg = OptimizerConfig()
+    far = F.VectorField._wrap(g, -100.0 * grad.data)
+    gamma, _, j_new = armijo_line_search(model, far, grad, cfg)
+    assert gamma is not None and gamma < 1.0
+    assert j_new <= model.objective() + cfg.armijo_c1 * gamma * F.l2_inner(grad, far)
+
+
+def test_objective_and_pure_distance_at_rest():
+    from paper_2401_17493_b200.distance import dist_value
+
+    m0, m1, _ = F.synth_case("translation", 32, seed=0)
+    st = F.KktState(m0, m1, plain(1e-2))
+    assert st.objective() == pytest.approx(dist_value(m0, m1, "ssd"), rel=1e-14)
+    g = F.Grid((32, 32), n_t=2)
+    const = F.ScalarField.full(g, 0.5)
+    st = F.KktState(const, const, plain(0.3))
+    v = F.VectorField(g, np.stack([np.sin(2 * _coords(g)[0]), np.zeros(g.n)]))
+    st.refresh(v)
+    # a single mode k = (2, 0): (alpha / 2) |k|^2 <v, v>
+    assert st.objective() == pytest.approx(0.5 * 0.3 * 4.0 * F.l2_inner(v, v), rel=1e-12)
+
+
+def test_functional_aliases_delegate_to_the_state(rng):
+    from paper_2401_17493_b200 import kkt as K
+
+    m0, m1, _ = F.synth_case("rotation", 32, seed=3)
+    st = F.KktState(m0, m1, plain(1e-2))
+    assert K.evaluate_objective(st) == st.objective()
+    vt = bandlimited(st.grid, rng, amp=0.4)
+    assert K.evaluate_objective(st, vt) == pytest.approx(st.objective_at(vt), rel=1e-14)
+    assert torch.equal(K.evaluate_gradient(st).data, st.gradient().data)
+    assert float((K.hessian_matvec_gn(st, vt).data - st.hessian_matvec(vt).data).abs().max()) < 1e-14
+    r = bandlimited(st.grid, rng)
+    assert torch.equal(K.apply_precond(r, F.PrecondKind("reg"), st).data,
+                       apply_inv_reg_operator(r, F.RegOperatorSpec(), 1e-2).data)
+
+
+def test_register_objective_monotone_and_counter_identity():
+    m0, m1, _ = F.synth_case("rotation", 64, seed=2)
+    _, rep = F.register(m0, m1, reg=plain(1e-2), precond=F.PrecondKind("reg"))
+    obj = [row["objective"] for row in rep.trace]
+    assert all(b <= a + 1e-12 for a, b in zip(obj, obj[1:]))
+    assert rep.pde_solves == 2 * (rep.iterations + 1) + 2 * rep.matvecs + rep.line_search_evals
+    assert len(rep.trace) == rep.iterations + 1
+
+
+def test_register_reports_are_deterministic():
+    m0, m1, _ = F.synth_case("translation", 32, seed=3)
+    d1 = F.register(m0, m1, reg=plain(1e-2))[1].to_dict()
+    d2 = F.register(m0, m1, reg=plain(1e-2))[1].to_dict()
+    d1.pop("runtime"), d2.pop("runtime")
+    for row in d1["trace"] + d2["trace"]:
+        row.pop("time", None)
+    assert d1 == d2
+
+
+@pytest.mark.parametrize("tdt", [None, np.float32])
+def test_register_variants_converge(tdt):
+    # NCC on a translation, 3D, the all-spectral derivative scheme
+    m0, m1, _ = F.synth_case("translation", 64, seed=0)
+    _, rep = F.register(m0, m1, reg=plain(1e-2), distance="ncc", precond=F.PrecondKind("h0"), transport_dtype=tdt)
+    assert rep.mismatch <= 0.1
+    m0, m1, _ = F.synth_case("rotation", 32, seed=1, d=3)
+    _, rep = F.register(m0, m1, reg=plain(1e-2), precond=F.PrecondKind("h0"), transport_dtype=tdt)
+    assert rep.status == "converged" and rep.mismatch <= 0.2 and rep.detgrad_min > 0.0
+    m0, m1, _ = F.synth_case("rotation", 32, seed=2)
+    _, rep = F.register(m0, m1, reg=plain(1e-2), precond=F.PrecondKind("h0"), scheme="spectral",
+                        transport_dtype=tdt)
+    assert rep.status == "converged" and rep.mismatch <= 0.1
+
+
+def test_divergence_control_tightens_volume_change():
+    m0, m1, _ = F.synth_case("swirl", 64, seed=1)
+    _, free = F.register(m0, m1, reg=plain(1e-2), precond=F.PrecondKind("h0"))
+    hard_reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("incompressible"))
+    _, hard = F.register(m0, m1, reg=hard_reg, precond=F.PrecondKind("h0"))
+    assert hard.status == "converged" and hard.mismatch <= 0.15
+    assert hard.detgrad_min > 0.9 and hard.detgrad_max < 1.1
+    assert hard.detgrad_max - hard.detgrad_min < free.detgrad_max - free.detgrad_min
+    assert free.divergence_energy == 0.0
+    soft_reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    _, soft = F.register(m0, m1, reg=soft_reg, precond=F.PrecondKind("h0"))
+    assert soft.divergence_energy > 0.0
