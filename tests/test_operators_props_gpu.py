@@ -497,3 +497,61 @@ def test_cascade_schedule_and_single_stage_target():
     assert len(stages) == 1 and rep.mismatch == pytest.approx(direct.mismatch, rel=1e-12)
     with pytest.raises(ValueError):
         F.continuation_solve(m0, m1, 0.0)
+
+
+def _plain(alpha=1.0):
+    return F.RegConfig(alpha=alpha, incomp=F.IncompressibilityMode("none"))
+
+
+def test_search_brackets_the_compress_pair_and_passes(tmp_path):
+    from paper_2401_17493_b200.continuation import write_trials_csv
+
+    m0, m1, _ = F.synth_case("compress", 64, seed=0)
+    cfg = F.SearchConfig(bisection_depth=4)
+    res = F.search_alpha(m0, m1, cfg=cfg, reg=_plain(), precond=F.PrecondKind("h0"))
+    assert res.status == "ok" and res.alpha is not None
+    assert F.det_bounds_ok(res.velocity, cfg.eps_det)[0]
+    assert res.anomalies == []
+    largest_fail = max(t.alpha for t in res.trials if not t.passed)
+    assert all(t.passed for t in res.trials if t.alpha > largest_fail)
+    assert all(t.warm_started or t.alpha == 1.0 or t.warm_start_dropped for t in res.trials)
+    sweep = [t for t in res.trials if t.phase == "sweep"]
+    assert not sweep[-1].passed and all(t.passed for t in sweep[:-1])
+    write_trials_csv(tmp_path / "trials.csv", res.trials)
+    assert (tmp_path / "trials.csv").read_text().splitlines()[0].startswith("alpha,passed,det_min,det_max")
+
+
+def test_search_edge_cases():
+    m0, m1, _ = F.synth_case("rotation", 32, seed=2)
+    res = F.search_alpha(m0, m1, cfg=F.SearchConfig(eps_det=0.999999, bisection_depth=2), reg=_plain())
+    assert res.status == "violated_at_start" and res.alpha is None
+    assert len(res.trials) == 1 and not res.trials[0].passed
+    res = F.search_alpha(m0, m1, cfg=F.SearchConfig(alpha_floor=1e-2), reg=_plain(), precond=F.PrecondKind("h0"))
+    assert res.status == "floor_reached" and res.alpha == pytest.approx(1e-2)
+    assert all(t.passed for t in res.trials)
+
+
+def test_warm_cascade_at_least_as_good_as_cold():
+    m0, m1, _ = F.synth_case("swirl", 64, seed=1)
+    _, cold = F.register(m0, m1, reg=_plain(1e-2), precond=F.PrecondKind("h0"))
+    _, rep, stages = F.continuation_solve(m0, m1, 1e-2, reg=_plain(), precond=F.PrecondKind("h0"))
+    assert len(stages) == 3 and rep.mismatch <= cold.mismatch * 1.05
+    assert rep.pde_solves == sum(s.pde_solves for s in stages)
+    assert rep.iterations == sum(s.iterations for s in stages)
+
+
+def test_preconditioner_iteration_ordering_at_small_alpha():
+    from paper_2401_17493_b200.optimizer import OptimizerConfig, pcg_newton_step
+
+    m0, m1, _ = F.synth_case("swirl", 64, seed=1)
+    reg = _plain(1e-3)
+    v, _ = F.register(m0, m1, reg=reg, precond=F.PrecondKind("h0"))
+    counts = {}
+    for kind in ("2level", "h0", "reg"):
+        st = F.KktState(m0, m1, reg)
+        st.refresh(v)
+        _, n, info = pcg_newton_step(st, st.gradient(), F.PrecondKind(kind), 1e-6,
+                                     OptimizerConfig(pcg_max_iterations=2000))
+        assert info["flag"] == "converged"
+        counts[kind] = n
+    assert counts["2level"] <= counts["h0"] <= counts["reg"]
