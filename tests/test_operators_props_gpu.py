@@ -555,3 +555,25 @@ def test_preconditioner_iteration_ordering_at_small_alpha():
         assert info["flag"] == "converged"
         counts[kind] = n
     assert counts["2level"] <= counts["h0"] <= counts["reg"]
+
+
+def test_mesh_coordinates_tile_the_box_and_containers_copy():
+    g3 = F.Grid((8, 8, 8))
+    assert np.allclose(F.mesh_coordinates(g3, (3, 4, 5)), (np.pi / 4, 0.0, -np.pi / 4))
+    g = F.Grid((8, 10))
+    with pytest.raises(IndexError):
+        F.mesh_coordinates(g, (3, 11))
+    raw = [F.mesh_coordinates(g, (a, b)) for a in range(1, 9) for b in range(1, 11)]
+    assert all(-np.pi <= p[0] < np.pi and -np.pi <= p[1] < np.pi for p in raw)
+    pts = {tuple(np.round(p, 12)) for p in raw}
+    assert len(pts) == 80
+    assert np.allclose(np.diff(sorted({p[0] for p in pts})), g.h[0])
+    gt = F.Grid((8, 8), n_t=2)
+    s = F.ScalarField.zeros(gt)
+    ts = F.TimeSeriesField.from_slices(gt, [s, s, s])
+    ts.slice(0).values[0, 0] = 99.0
+    assert float(ts.data[0, 0, 0]) == 0.0
+    s.values[0, 0] = 7.0
+    assert float(ts.data[0, 0, 0]) == 0.0
+    with pytest.raises(ValueError):
+        F.VectorField.from_components([F.ScalarField.zeros(F.Grid((8, 8))), F.ScalarField.zeros(F.Grid((16, 16)))])
