@@ -155,6 +155,7 @@ struct KktCtx {
     DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
     DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
     bool gy_ready = false;  // grads_y (grad m_j at the forward feet) matches the current state
+    bool grad0_ready = false;  // grads slice 0 = grad m0: fixed by set_images, reused by every refresh
     bool coarse_ready = false, h0_ready = false;
     bool have_images = false, have_state = false;
     double initial_mismatch = 0.0, dist_cur = 0.0;
@@ -308,6 +309,7 @@ void kkt_set_images(KktCtx* k, const void* m0, const void* m1, int dtype) {
     convert(dtype, m1, k->tdt, k->m1.p, k->N(), k->st);
     k->tmp1.alloc(k->N() * k->T());
     k->have_images = true;
+    k->grad0_ready = false;
     k->initial_mismatch = dist_value(k, k->m0.p);
 }
 
@@ -377,7 +379,14 @@ void kkt_refresh(KktCtx* k, const void* v) {
         spectral_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
     FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
     solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);         // kkt.py:174
-    gradient_slices(k, k->n_t + 1, k->mseries.p, k->grads.p);                              // kkt.py:175
+    // kkt.py:175; slice 0 is m0 itself, whose gradient the first refresh
+    // after set_images computed (per-slice results do not depend on the batch)
+    if (k->grad0_ready) {
+        gradient_slices(k, k->n_t, k->mseries.at<char>(N * T), k->grads.at<char>((size_t)d * N * T));
+    } else {
+        gradient_slices(k, k->n_t + 1, k->mseries.p, k->grads.p);
+        k->grad0_ready = true;
+    }
     // grad m_j at the forward feet (transport.py:172) is only read by the GN
     // matvec: gathered by its first call after this refresh (ensure_grads_y),
     // so the refresh that ends a solve — no matvec follows — skips it
