@@ -155,7 +155,7 @@ struct KktCtx {
     DevBuf c_gm, c_w, c_x, c_r, c_z, c_s, c_q, c_u;
     DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
     bool gy_ready = false;  // grads_y (grad m_j at the forward feet) matches the current state
-    bool grad0_ready = false;  // grads slice 0 = grad m0: fixed by set_images, reused by every refresh
+    bool grad0_ready = false;  // mseries / grads slice 0 = m0 / grad m0: fixed by set_images, kept by refreshes
     bool coarse_ready = false, h0_ready = false;
     bool have_images = false, have_state = false;
     double initial_mismatch = 0.0, dist_cur = 0.0;
@@ -377,7 +377,7 @@ void kkt_refresh(KktCtx* k, const void* v) {
         fd8_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
     else
         spectral_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
-    FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
+    if (!k->grad0_ready) FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
     solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);         // kkt.py:174
     // kkt.py:175; slice 0 is m0 itself, whose gradient the first refresh
     // after set_images computed (per-slice results do not depend on the batch)
