@@ -138,6 +138,15 @@ struct DevBuf {
     }
 };
 
+// flag = 1 if the two word arrays differ anywhere (bitwise)
+__global__ void k_words_differ(const unsigned* __restrict__ a, const unsigned* __restrict__ b, long long n,
+                               int* __restrict__ flag) {
+    bool diff = false;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        diff |= a[i] != b[i];
+    if (__syncthreads_or(diff) && threadIdx.x == 0) *flag = 1;
+}
+
 struct KktCtx {
     Dims g;
     int n_t, method, scheme, distance, tdt, cdt;
@@ -156,6 +165,11 @@ struct KktCtx {
     DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
     bool gy_ready = false;  // grads_y (grad m_j at the forward feet) matches the current state
     bool grad0_ready = false;  // mseries / grads slice 0 = m0 / grad m0: fixed by set_images, kept by refreshes
+    // the last objective_at's departure map (disp_trial) was built from the
+    // transport-precision velocity still held in vtT: a refresh at that same
+    // velocity (the accepted Armijo trial) takes the map instead of rebuilding it
+    bool trial_map_valid = false;
+    DevBuf flag;
     bool coarse_ready = false, h0_ready = false;
     bool have_images = false, have_state = false;
     double initial_mismatch = 0.0, dist_cur = 0.0;
@@ -357,6 +371,24 @@ void kkt_set_interp_bits(KktCtx* k, int bits) {
     k->interp_bits = bits;
 }
 
+// whether disp_trial is the forward map of the velocity now in vT: the last
+// objective_at built it from vtT (nothing wrote either since) and vtT == vT
+// bit for bit (one read of both, one 4-byte readback)
+static bool trial_map_matches(KktCtx* k) {
+    static const bool off = getenv("FRG_NO_TRIAL_REUSE") != nullptr;
+    if (off || !k->trial_map_valid || k->cdt == k->tdt) return false;
+    const long long words = (long long)k->g.d * k->N() * k->T() / 4;
+    k->flag.alloc(sizeof(int));
+    FRG_CUDA(cudaMemsetAsync(k->flag.p, 0, sizeof(int), k->st));
+    k_words_differ<<<blocks_for(words / 4, 256) < 4 * 148 ? blocks_for(words / 4, 256) : 4 * 148, 256, 0, k->st>>>(
+        (const unsigned*)k->vT.p, (const unsigned*)k->vtT.p, words, k->flag.at<int>());
+    FRG_CHECK_LAUNCH();
+    int differ = 1;
+    FRG_CUDA(cudaMemcpyAsync(&differ, k->flag.p, sizeof(int), cudaMemcpyDeviceToHost, k->st));
+    FRG_CUDA(cudaStreamSynchronize(k->st));
+    return differ == 0;
+}
+
 void kkt_refresh(KktCtx* k, const void* v) {
     FRG_REQUIRE(k->have_images, "set_images must precede refresh");
     k->obj_valid = false;
@@ -366,7 +398,14 @@ void kkt_refresh(KktCtx* k, const void* v) {
     FRG_CUDA(cudaMemcpyAsync(k->v.p, v, d * N * C, cudaMemcpyDeviceToDevice, st));
     // vT = v in transport precision (departure + divergence)
     convert(k->cdt, k->v.p, k->tdt, k->vT.p, d * N, st);
-    departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->vT.p, k->disp_f.p, st);   // kkt.py:171
+    if (trial_map_matches(k)) {
+        // bit-identical to departure(vT): the same kernel on the same input (a
+        // copy, not a pointer swap: the small-grid matvec graph is keyed on disp_f)
+        FRG_CUDA(cudaMemcpyAsync(k->disp_f.p, k->disp_trial.p, d * N * T, cudaMemcpyDeviceToDevice, st));
+    } else {
+        departure(k->g, k->tdt, k->tdt, k->method, 1.0 / k->n_t, k->vT.p, k->disp_f.p, st);  // kkt.py:171
+    }
+    k->trial_map_valid = false;
     // departure map of -v (kkt.py:172) without a negated copy: the step -h_t
     // flips the sign of every displacement and of the gathered v, which is
     // bit-identical to transporting a negated field
@@ -451,6 +490,7 @@ double kkt_objective_at(KktCtx* k, const void* v_trial) {
     const size_t T = k->T();
     // fresh trajectory + state solve keeping only two slices (kkt.py:201-205)
     departure_of(k, v_trial, k->disp_trial.p, k->vtT.p, false);
+    k->trial_map_valid = k->cdt != k->tdt;  // departure_of staged the fp32 trial velocity in vtT
     PlanScope pt(0, k->disp_trial.p, build_plan(k, k->disp_trial.p, k->plan_t), k->method);
     FRG_CUDA(cudaMemcpyAsync(k->mtrial.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, k->st));
     for (int j = 0; j < k->n_t; ++j) {
@@ -561,6 +601,7 @@ static std::vector<const void*> graph_key(KktCtx* k) {
 
 void kkt_hessian_matvec(KktCtx* k, const void* vt, void* out) {
     FRG_REQUIRE(k->have_state, "refresh first");
+    k->trial_map_valid = false;  // the matvec stages v~ in vtT
     ensure_grads_y(k);  // eager, never inside the small-grid graph capture
     const size_t bytes = (size_t)k->g.d * k->N() * k->C();
     if (graph_ok(k) && ++k->mv_calls >= 2) {  // the first call allocates every workspace the sequence uses

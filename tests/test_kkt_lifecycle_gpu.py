@@ -47,3 +47,34 @@ def test_refreshed_context_equals_fresh_context(n, tdt):
     assert all(torch.equal(h, want) for h in got)
     assert torch.equal(g_got, fresh.gradient().data)
     assert st.objective() == fresh.objective()
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_refresh_at_the_accepted_trial_reuses_its_map_bit_for_bit(n):
+    """A refresh at the velocity of the last objective_at (the accepted Armijo
+    trial) takes that trial's departure map instead of rebuilding it (mixed
+    precision; csrc/kkt.cu trial_map_matches); a matvec in between, or a
+    different velocity, falls back to building it.  Either way the state is
+    bit-identical to a fresh context's."""
+    import paper_2401_17493_b200 as F
+
+    m0, m1, vtrue = F.synth_case("rotation", n, seed=1, d=3)
+    grid = m0.grid
+    reg = F.RegConfig(alpha=1e-2, incomp=F.IncompressibilityMode("near-incompressible", 1e-4))
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    vt = F.VectorField._wrap(grid, 0.1 * torch.randn((3, n, n, n), generator=gen, dtype=torch.float64,
+                                                     device="cuda"))
+    v1 = F.VectorField._wrap(grid, 0.3 * vtrue.data)
+    v2 = F.VectorField._wrap(grid, 0.55 * vtrue.data)
+    st = F.KktState(m0, m1, reg, v_init=v1, transport_dtype=np.float32)
+    for sequence in ("accepted", "matvec-between", "other-velocity"):
+        st.objective_at(v2)
+        if sequence == "matvec-between":
+            st.hessian_matvec(vt)
+        target = v2 if sequence != "other-velocity" else v1
+        st.refresh(target)
+        fresh = F.KktState(m0, m1, reg, v_init=target, transport_dtype=np.float32)
+        assert torch.equal(st.gradient().data, fresh.gradient().data), sequence
+        assert torch.equal(st.hessian_matvec(vt).data, fresh.hessian_matvec(vt).data), sequence
+        assert st.objective() == fresh.objective(), sequence
+        st.refresh(v1)
