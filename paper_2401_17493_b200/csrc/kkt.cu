@@ -136,6 +136,10 @@ struct DevBuf {
     T* at(size_t byte_off = 0) const {
         return (T*)((char*)p + byte_off);
     }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+    }
 };
 
 // flag = 1 if the two word arrays differ anywhere (bitwise)
@@ -165,9 +169,10 @@ struct KktCtx {
     DevBuf pre32;  // mixed-precision 'reg' preconditioner: fp32 copy of r / z
     bool gy_ready = false;  // grads_y (grad m_j at the forward feet) matches the current state
     bool grad0_ready = false;  // mseries / grads slice 0 = m0 / grad m0: fixed by set_images, kept by refreshes
-    // the last objective_at's departure map (disp_trial) was built from the
-    // transport-precision velocity still held in vtT: a refresh at that same
-    // velocity (the accepted Armijo trial) takes the map instead of rebuilding it
+    // the last objective_at's departure map (disp_trial) and state series
+    // (mtrial) were built from the transport-precision velocity still held in
+    // vtT: a refresh at that same velocity (the accepted Armijo trial) takes
+    // both instead of rebuilding them
     bool trial_map_valid = false;
     DevBuf flag;
     bool coarse_ready = false, h0_ready = false;
@@ -236,7 +241,7 @@ KktCtx* kkt_create(const Dims& g, int n_t, int method, int scheme, int distance,
     k->lt.alloc((n_t + 1) * N * T);
     k->bf.alloc(d * N * T);
     k->disp_trial.alloc(d * N * T);
-    k->mtrial.alloc(2 * N * T);
+    k->mtrial.alloc((n_t + 1) * N * T);  // the trial's whole state series: a refresh at it takes the series
     size_t sa = (size_t)half_len(g) * (C == 8 ? 16 : 8) * d + (size_t)half_len(g) * 8;
     size_t sb = (size_t)half_len(g) * (T == 8 ? 16 : 8) * d;
     k->ws_a.get(sa);
@@ -324,6 +329,7 @@ void kkt_set_images(KktCtx* k, const void* m0, const void* m1, int dtype) {
     k->tmp1.alloc(k->N() * k->T());
     k->have_images = true;
     k->grad0_ready = false;
+    k->trial_map_valid = false;  // a trial's state series was solved from the previous m0
     k->initial_mismatch = dist_value(k, k->m0.p);
 }
 
@@ -398,7 +404,8 @@ void kkt_refresh(KktCtx* k, const void* v) {
     FRG_CUDA(cudaMemcpyAsync(k->v.p, v, d * N * C, cudaMemcpyDeviceToDevice, st));
     // vT = v in transport precision (departure + divergence)
     convert(k->cdt, k->v.p, k->tdt, k->vT.p, d * N, st);
-    if (trial_map_matches(k)) {
+    const bool from_trial = trial_map_matches(k);
+    if (from_trial) {
         // bit-identical to departure(vT): the same kernel on the same input (a
         // copy, not a pointer swap: the small-grid matvec graph is keyed on disp_f)
         FRG_CUDA(cudaMemcpyAsync(k->disp_f.p, k->disp_trial.p, d * N * T, cudaMemcpyDeviceToDevice, st));
@@ -416,8 +423,13 @@ void kkt_refresh(KktCtx* k, const void* v) {
         fd8_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
     else
         spectral_divergence(k->g, k->tdt, k->vT.p, k->divv.p, st);
-    if (!k->grad0_ready) FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
-    solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);         // kkt.py:174
+    if (from_trial) {
+        // the trial solved this very state on the same map (slice 0 = m0)
+        k->mseries.swap(k->mtrial);
+    } else {
+        if (!k->grad0_ready) FRG_CUDA(cudaMemcpyAsync(k->mseries.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, st));
+        solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_f.p, k->mseries.p, st);     // kkt.py:174
+    }
     // kkt.py:175; slice 0 is m0 itself, whose gradient the first refresh
     // after set_images computed (per-slice results do not depend on the batch)
     if (k->grad0_ready) {
@@ -492,14 +504,12 @@ double kkt_objective_at(KktCtx* k, const void* v_trial) {
     departure_of(k, v_trial, k->disp_trial.p, k->vtT.p, false);
     k->trial_map_valid = k->cdt != k->tdt;  // departure_of staged the fp32 trial velocity in vtT
     PlanScope pt(0, k->disp_trial.p, build_plan(k, k->disp_trial.p, k->plan_t), k->method);
+    // the whole series (same writes as a ping-pong pair): a refresh at this
+    // velocity swaps it in as its state instead of re-solving (refresh)
     FRG_CUDA(cudaMemcpyAsync(k->mtrial.p, k->m0.p, N * T, cudaMemcpyDeviceToDevice, k->st));
-    for (int j = 0; j < k->n_t; ++j) {
-        const void* in = k->mtrial.at<char>((size_t)(j & 1) * N * T);
-        void* out = k->mtrial.at<char>((size_t)((j + 1) & 1) * N * T);
-        gather_fields(k->g, k->tdt, k->method, k->disp_trial.p, 1, &in, &out, k->st);
-    }
+    solve_state(k->g, k->tdt, k->method, k->n_t, k->disp_trial.p, k->mtrial.p, k->st);
     k->pde_solves += 1;
-    const void* mfin = k->mtrial.at<char>((size_t)(k->n_t & 1) * N * T);
+    const void* mfin = k->mtrial.at<char>((size_t)k->n_t * N * T);
     return dist_value(k, mfin) + reg_energy_c(k, v_trial);
 }
 
