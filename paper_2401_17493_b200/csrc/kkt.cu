@@ -386,8 +386,9 @@ static bool trial_map_matches(KktCtx* k) {
     const long long words = (long long)k->g.d * k->N() * k->T() / 4;
     k->flag.alloc(sizeof(int));
     FRG_CUDA(cudaMemsetAsync(k->flag.p, 0, sizeof(int), k->st));
-    k_words_differ<<<blocks_for(words / 4, 256) < 4 * 148 ? blocks_for(words / 4, 256) : 4 * 148, 256, 0, k->st>>>(
-        (const unsigned*)k->vT.p, (const unsigned*)k->vtT.p, words, k->flag.at<int>());
+    const int nblk = (int)std::max(1LL, std::min((long long)blocks_for(words / 4, 256), 4LL * 148));
+    k_words_differ<<<nblk, 256, 0, k->st>>>((const unsigned*)k->vT.p, (const unsigned*)k->vtT.p, words,
+                                            k->flag.at<int>());
     FRG_CHECK_LAUNCH();
     int differ = 1;
     FRG_CUDA(cudaMemcpyAsync(&differ, k->flag.p, sizeof(int), cudaMemcpyDeviceToHost, k->st));
